@@ -1,0 +1,421 @@
+"""Benchmark: fused EmbeddingBag(sum) + All-to-All on B200 vs the unfused pool + NCCL baseline.
+
+Metric (BASELINE.json): "fused emb+All-to-All us & lookups/s at 1/2/4/8 B200 vs unfused
+emb+NCCL".  One step = one fused forward (rows a1-a8: pool this rank's tables for the whole
+global batch, zero-copy store to every destination, signal, receive wait) over one batch.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dlrm_small] [--impl fused|reference]
+
+N=1 runs the config's per-rank work at W=1; under torchrun each rank
+owns one GPU and the config runs at W=N (W-scaling rule: T_r, rows, D, B, pooling fixed).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0      # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json absent)
+NVLINK_GBS = 770.0             # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+L2_FLUSH_BYTES = 512 << 20     # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="dlrm_small")
+    ap.add_argument("--impl", default="fused", choices=["fused", "reference"])
+    ap.add_argument("--alpha", type=float, default=1.05)
+    ap.add_argument("--slice", type=int, default=0, help="slice size S (0 = library default)")
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--unroll", type=int, default=0)
+    ap.add_argument("--order", type=int, default=-1)
+    ap.add_argument("--batches", type=int, default=8, help="distinct pre-generated batches")
+    ap.add_argument("--no-baseline", action="store_true", help="skip the unfused NCCL baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg):
+    kind, p = cfg.pool
+    pool = f"L={p}" if kind == "fixed" else f"L~U{{1..{2 * p - 1}}}"
+    return (f"{cfg.name} at W={cfg.W}: {cfg.T[0]} tables/rank x {cfg.R} rows x D={cfg.D}, "
+            f"global batch {cfg.B}, {pool}, Zipf alpha={cfg.alpha}, fp32")
+
+
+def algorithmic_bytes(cfg, r, nnz):
+    """Per-rank algorithmic bytes of one forward: gathered rows + indices +
+    offsets + this rank's receive buffer; and the bytes it must send over NVLink."""
+    b = int(cfg.part[r + 1] - cfg.part[r])
+    T = cfg.T[r]
+    hbm = nnz * cfg.D * 4 + nnz * 4 + (T * cfg.B + 1) * 4 + b * cfg.G * cfg.D * 4
+    tx = (cfg.B - b) * T * cfg.D * 4
+    return hbm, tx
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle timing
+
+def oracle_pass(cfg, csr, rows_per_call=None):
+    """The oracle as it stands (single-threaded C): this rank-0 view of the workload = every
+    destination row of every rank's output, procedural tables.  Returns (lookups, seconds)."""
+    import oracle
+    idx = [c[0] for c in csr]
+    off = [c[1] for c in csr]
+    lookups, secs = 0, 0.0
+    for s in range(cfg.W):
+        b = int(cfg.part[s + 1] - cfg.part[s])
+        sel = np.arange(b) if rows_per_call is None else np.arange(min(b, rows_per_call))
+        t0 = time.perf_counter()
+        oracle.emb_a2a_rows(cfg.table_seed, cfg.value_mode, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
+                            idx, off, s, sel, check_inputs=False)
+        secs += time.perf_counter() - t0
+        for r in range(cfg.W):
+            o = off[r].astype(np.int64)
+            for t in range(cfg.T[r]):
+                js = cfg.part[s] + sel
+                lookups += int((o[t * cfg.B + js + 1] - o[t * cfg.B + js]).sum())
+    return lookups, secs
+
+
+def cpu_baseline(cfg, csr_batches, budget_s):
+    """Bounded sample: whole-batch oracle passes over the rotating batches until ~budget_s."""
+    lookups, secs, passes = 0, 0.0, 0
+    while secs < budget_s and passes < 64:
+        l, s = oracle_pass(cfg, csr_batches[passes % len(csr_batches)])
+        lookups += l
+        secs += s
+        passes += 1
+    return {"value": lookups / secs, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+            "sample": f"{passes} full forward(s) of the workload ({lookups} lookups, "
+                      f"{secs:.2f} s, single-threaded C oracle, procedural tables)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle is this tier's reference arm (no installable reference
+    exists; PAPER.md ships no code).  Rank 0 only."""
+    import synth
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    N = max(args.gpus, world)
+    cfg = synth.config_for(args.config, W=N, alpha=args.alpha)
+    csrs = [synth.gen_all_csr(cfg, k) for k in range(min(args.batches, 2))]
+    for w in range(args.warmup):
+        oracle_pass(cfg, csrs[w % len(csrs)], rows_per_call=8)
+    lookups, secs = 0, 0.0
+    for k in range(args.steps):
+        l, s = oracle_pass(cfg, csrs[k % len(csrs)])
+        lookups += l
+        secs += s
+    v = lookups / secs
+    line = {"metric": "fused emb+All-to-All lookups/s", "value": v, "unit": "lookups/s",
+            "impl": "reference", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "global_batch": cfg.B,
+                       "tables_per_rank": cfg.T[0], "rows": cfg.R, "dim": cfg.D},
+            "cpu_baseline": {"value": v, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full forwards of the workload (all W ranks' "
+                                       "outputs), single-threaded C oracle"},
+            "e2e": {"value": v, "unit": "lookups/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import synth.device as sdev
+    from paper_2305_06942_b200 import EmbA2A, torch_allgather
+
+    rank, world, local = dist_env()
+    N = world
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            import socket
+            s = socket.socket()
+            s.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+            s.close()
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+    cfg = synth.config_for(args.config, W=N, alpha=args.alpha)
+    # ---- inputs (all resident in HBM before timing; 8 rotating batches)
+    csr_batches = [synth.gen_all_csr(cfg, k) if rank == 0 and not args.no_cpu and N == 1
+                   else None for k in range(args.batches)]
+    mine = []
+    for k in range(args.batches):
+        idx, off = (csr_batches[k][rank] if csr_batches[k] is not None
+                    else synth.gen_rank_csr(cfg, rank, k))
+        mine.append((idx, off))
+    d_in = [(torch.from_numpy(i).to(dev), torch.from_numpy(o).to(dev)) for i, o in mine]
+    h_in = [(torch.from_numpy(i).pin_memory(), torch.from_numpy(o).pin_memory()) for i, o in mine]
+    nnz_all = []   # global lookups per batch
+    for k in range(args.batches):
+        t = torch.tensor([mine[k][0].size], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        nnz_all.append(int(t.item()))
+    tables = sdev.rank_tables(cfg, rank, dev)
+    torch.cuda.synchronize()
+
+    h = EmbA2A(rank, N, dev, torch_allgather(None, dev))
+    if args.slice:
+        h.set_option("slice", args.slice)
+    if args.threads:
+        h.set_option("threads", args.threads)
+    if args.unroll:
+        h.set_option("unroll", args.unroll)
+    if args.order >= 0:
+        h.set_option("order", args.order)
+    h.register_tables(tables, cfg.B)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def timed_loop(step_fn, K, W, with_barrier=True):
+        """W warm-up steps, then K steps; per step: L2 flush, device barrier, events around the
+        step on the launching stream.  Returns per-step ms (this rank)."""
+        for w in range(W):
+            step_fn(w % args.batches)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
+        for k in range(K):
+            flush.zero_()
+            if with_barrier:
+                h.device_barrier(stream)
+            evs[k][0].record(stream)
+            step_fn(k % args.batches)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- fused (the product)
+    fused_step = lambda k: h.forward(d_in[k][0], d_in[k][1], stream)  # noqa: E731
+    launches0 = h.query("kernel_launches")
+    clk = ClockSampler(local)
+    clk.start()
+    ms = timed_loop(fused_step, args.steps, args.warmup)
+    clocks = clk.stop()
+    launches = h.query("kernel_launches") - launches0 - args.warmup
+    total_ms = max_over_ranks(sum(ms))
+    lookups = sum(nnz_all[k % args.batches] for k in range(args.steps))
+    value = lookups / (total_ms / 1e3)
+    ms_step = total_ms / args.steps
+
+    # dominant kernel = the fused kernel (one launch per step); per-launch time from the same events
+    nnz_mean = float(np.mean([mine[k % args.batches][0].size for k in range(args.steps)]))
+    hbm_b, tx_b = algorithmic_bytes(cfg, rank, nnz_mean)
+    kern_s = float(np.mean(ms)) / 1e3
+    peak_hbm, peak_src = measured_peaks()
+    t_hbm = hbm_b / (peak_hbm * 1e9)
+    t_nvl = tx_b / (NVLINK_GBS * 1e9)
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": tx_b / kern_s / 1e9, "peak": NVLINK_GBS,
+                "unit": "GB/s", "peak_source": "measured peer copy (B200_PROFILING.md)"}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_b / kern_s / 1e9, "peak": peak_hbm,
+                "unit": "GB/s", "peak_source": peak_src}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["algorithmic_bytes_per_launch"] = hbm_b
+    roof["nvlink_tx_bytes_per_launch"] = tx_b
+    roof["traffic"] = ncu_traffic(cfg)
+    roof["roofline_us"] = max(t_hbm, t_nvl) * 1e6
+
+    # ---- end to end through the public API: pinned host inputs -> device -> host result
+    b = h.b
+    h_out = torch.empty((b, h.G * h.D), dtype=torch.float32).pin_memory()
+    e2e_step = lambda k: h.forward_host(h_in[k][0], h_in[k][1], h_out, stream)  # noqa: E731
+    e2e_ms = timed_loop(e2e_step, args.steps, args.warmup)
+    e2e_total = max_over_ranks(sum(e2e_ms))
+    h2d = float(np.mean([(mine[k % args.batches][0].size + mine[k % args.batches][1].size) * 4
+                         for k in range(args.steps)]))
+    e2e = {"value": lookups / (e2e_total / 1e3), "unit": "lookups/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(b * h.G * h.D * 4),
+           "ms_per_step": e2e_total / args.steps}
+
+    # ---- unfused baseline: same pooling kernel -> staging, then NCCL all_to_all_single
+    unfused = None
+    if not args.no_baseline:
+        T = cfg.T[rank]
+        send = torch.empty((cfg.B, T, cfg.D), dtype=torch.float32, device=dev)
+        recv = torch.empty((N, b, T, cfg.D), dtype=torch.float32, device=dev)
+        final = torch.empty((b, cfg.G * cfg.D), dtype=torch.float32, device=dev)
+
+        def unfused_step(k, permute):
+            h.pool_local(d_in[k][0], d_in[k][1], send, stream)
+            dist.all_to_all_single(recv.view(-1), send.view(-1))
+            if permute:   # [src][i][t][d] -> [i][src*T+t][d] (R#17)
+                final.view(b, N, T, cfg.D).copy_(recv.permute(1, 0, 2, 3))
+
+        un_np = timed_loop(lambda k: unfused_step(k, False), args.steps, args.warmup)
+        un_p = timed_loop(lambda k: unfused_step(k, True), args.steps, args.warmup)
+        un_np_ms = max_over_ranks(sum(un_np)) / args.steps
+        un_p_ms = max_over_ranks(sum(un_p)) / args.steps
+        # parity of the two paths on the last batch (cheap, outside timing)
+        k = 0
+        out_f = h.forward(d_in[k][0], d_in[k][1], stream).clone()
+        unfused_step(k, True)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(out_f, final))
+        unfused = {"us_no_permute": un_np_ms * 1e3, "us_with_permute": un_p_ms * 1e3,
+                   "lookups_per_s_no_permute": lookups / (un_np_ms * args.steps / 1e3),
+                   "fused_speedup_vs_no_permute": un_np_ms / ms_step,
+                   "fused_speedup_vs_permute": un_p_ms / ms_step,
+                   "fused_equals_unfused_bitwise": same}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, [c for c in csr_batches if c is not None], args.cpu_seconds)
+
+    line = {
+        "metric": "fused emb+All-to-All lookups/s (us/step in ms_per_step)",
+        "value": value, "unit": "lookups/s", "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "us_per_step": ms_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Zipf indices, procedural fp32 tables; DESIGN.md Input recipe)",
+        "config": {"workload": workload_desc(cfg), "global_batch": cfg.B,
+                   "tables_per_rank": cfg.T[0], "rows": cfg.R, "dim": cfg.D,
+                   "pooling": list(cfg.pool), "alpha": cfg.alpha, "world": N,
+                   "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
+                   "slice": h.get_option("slice"), "threads": h.get_option("threads"),
+                   "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+                   "batches": args.batches, "step_timing": "CUDA events around each forward "
+                   "after a cross-rank device barrier; sum over K steps; max over ranks"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
+        "clocks": clocks, "gpu_launches": int(launches),
+        "fused_us_p50": float(np.median(ms)) * 1e3, "fused_us_p90": float(np.percentile(ms, 90)) * 1e3,
+    }
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+    h.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def ncu_traffic(cfg):
+    """DRAM bytes per fused launch from a committed ncu --set full capture, if one exists for
+    this workload (profiles/ncu_traffic.json written from the .ncu-rep by tools)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    key = f"{cfg.name}_W{cfg.W}"
+    v = d.get(key)
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * emb_a2a.h -- C ABI of libemba2a.so: fused EmbeddingBag(sum) + All-to-All for B200 (sm_100a).
+ *
+ * Method: arXiv 2305.06942 ("fusing computation with communication using GPU-initiated
+ * networking").  Citations: P:n = PAPER.md line n (with section); S:n = SPEC.md line n;
+ * R#n = reading n in DESIGN.md.
+ *
+ * What one forward computes: rank r owns T_r embedding tables (model
+ * parallel, P:68 / P:135) and sum-pools them for the WHOLE global batch B.  Pooled vector (t, j)
+ * belongs to the rank s with p_s <= j < p_{s+1} (contiguous batch blocks) and lands in
+ * row i = j - p_s, columns [(toff_r + t) * D, (toff_r + t + 1) * D) of s's output
+ * {local batch b_s, numTables G x D}.  The kernel stores every pooled vector straight
+ * into the destination GPU's receive buffer over NVLink ("zero-copy", Sec 3.3), signals
+ * one per-peer arrival counter per completed slice with system-scope release semantics
+ * (the PUT -> fence -> sliceRdy protocol of P:151), and waits for every peer's slices with
+ * acquire loads before it exits ("poll on ... sliceRdy flags before exiting").
+ *
+ * Conventions (all entry points):
+ *  - Every call returns an int status (emb_a2a_status).  0 = success.
+ *  - A call that fails validation returns before enqueuing any GPU work.
+ *  - Asynchronous device failures (receive-wait timeout) are recorded in a mapped host word and
+ *    returned by the NEXT call on the handle as EMB_A2A_ETIMEOUT; the handle is then poisoned
+ *    (every later call except destroy returns EMB_A2A_ESTATE).
+ *  - register_tables, forward, forward_host and destroy are COLLECTIVE: every rank of the group
+ *    calls them the same number of times in the same order (as with NCCL).
+ *  - A handle is not thread-safe.  Different handles may be used from different threads.
+ *  - emb_a2a_last_error() returns a human-readable message for the last failure on a handle.
+ */
+#ifndef EMB_A2A_H_
+#define EMB_A2A_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMB_A2A_ABI_VERSION 1
+#define EMB_A2A_MAX_WORLD 64
+
+typedef enum {
+    EMB_A2A_OK = 0,
+    EMB_A2A_EINVAL = 1,    /* bad argument / inconsistent metadata across ranks */
+    EMB_A2A_ESTATE = 2,    /* call out of order, or handle poisoned by an earlier failure */
+    EMB_A2A_ECUDA = 3,     /* a CUDA runtime call failed (message in last_error) */
+    EMB_A2A_ENOMEM = 4,    /* device or pinned host allocation failed */
+    EMB_A2A_EPEER = 5,     /* a peer's buffers cannot be mapped (no P2P / IPC path) */
+    EMB_A2A_EBOOT = 6,     /* the caller's all-gather callback failed */
+    EMB_A2A_ETIMEOUT = 7,  /* a peer never signalled within timeout_ms (P:151 drain) */
+    EMB_A2A_EINDEX = 8     /* validate mode: index out of range / malformed CSR */
+} emb_a2a_status;
+
+typedef struct emb_a2a emb_a2a_t;
+
+/* Caller-supplied all-gather over its process group (the bootstrap channel; S:86 problem
+ * record exchange).  send: nbytes; recv: world_size * nbytes, rank-ordered.  Return 0 on success.
+ * Called synchronously from inside init / register_tables / destroy. */
+typedef int (*emb_a2a_allgather_fn)(const void* send, void* recv, size_t nbytes, void* user);
+
+/* Create a handle for rank `rank` of `world_size` (1..EMB_A2A_MAX_WORLD) on CUDA device
+ * `cuda_device`.  Several handles may live in one process (virtual ranks for loopback tests),
+ * on the same or different devices.  *out receives the handle.  Not collective. */
+int emb_a2a_init(int rank, int world_size, int cuda_device, emb_a2a_allgather_fn allgather,
+                 void* user, emb_a2a_t** out);
+
+/* Register this rank's tables and the problem shape (collective).
+ *  num_local_tables  T_r >= 0 (may differ across ranks; G = sum_r T_r >= 1).
+ *  tables            host array of T_r DEVICE pointers, each row-major [rows[t]][dim] float32,
+ *                    16-byte aligned.  Borrowed: must stay valid and unchanged during forwards
+ *                    until destroy.  Table-wise model parallelism.
+ *  rows              host array of T_r row counts, 1 <= rows < 2^31.
+ *  dim               D, identical on all ranks, D % 4 == 0, 4 <= D <= 1024 (R#9).
+ *  global_batch      B >= 0, identical on all ranks.
+ *  batch_partition   host array of W+1 prefix sums p (p_0 = 0, p_W = B, non-decreasing),
+ *                    identical on all ranks; NULL = even split (requires B % W == 0) (R#1).
+ * Allocates the symmetric receive region (2 buffers [b_r][G*D] float32 + per-peer counters,
+ * P:178 "symmetric heap"), exports it with cudaIpcGetMemHandle, maps every peer's region
+ * (cudaIpcOpenMemHandle; raw pointer for handles in the same process) -- the roc_shmem_ptr
+ * analogue of P:165 -- and all-gathers metadata to check consistency.
+ * May be called again to re-register (the old registration is torn down collectively). */
+int emb_a2a_register_tables(emb_a2a_t* h, int num_local_tables, const float* const* tables,
+                            const int64_t* rows, int dim, int64_t global_batch,
+                            const int64_t* batch_partition);
+
+/* One fused forward (collective), asynchronous on `stream` (cudaStream_t; NULL = legacy default).
+ *  indices   DEVICE int32[num_indices]: the T_r tables' bags concatenated table-major; values
+ *            are local row ids (0 <= idx < rows[t]).  Borrowed until the stream passes the op.
+ *  offsets   DEVICE int32[T_r * B + 1]: absolute CSR offsets, offsets[0] = 0, non-decreasing,
+ *            offsets[T_r*B] = num_indices (bag (t, j) = indices[offsets[t*B+j] .. offsets[t*B+j+1])).
+ *  out       receives a DEVICE pointer to this rank's output [b_r][G*D] float32 row-major, the
+ *            layout the interaction op consumes.  Library-owned; valid until the SECOND
+ *            following forward on this handle or destroy (double buffer by epoch parity).
+ *  out_rows, out_cols  receive b_r and G*D (either may be NULL).
+ * Preconditions (fast path, unchecked unless set_option("validate",1)): indices in range,
+ * offsets well formed.  The consumer of *out must be ordered before this rank's forward after
+ * next (same stream, or an event) -- DESIGN.md "Buffer-reuse proof". */
+int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                    int64_t num_indices, void* stream, float** out, int64_t* out_rows,
+                    int64_t* out_cols);
+
+/* The same forward fed from HOST memory (the end-to-end path): copies h_indices / h_offsets
+ * (host, ideally pinned) into library-owned device staging, runs the fused forward, and copies
+ * the [b_r][G*D] float32 result into h_out (host, b_r*G*D floats), all enqueued on `stream`.
+ * Returns after enqueuing; synchronise the stream before reading h_out (collective). */
+int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
+                         int64_t num_indices, void* stream, float* h_out);
+
+/* Unfused baseline, first half (not collective): the same pooling, written with local stores to
+ * a caller-owned DEVICE staging buffer `send`, dest-major [W][b_s][T_r][D] float32 (the block of
+ * destination s starts at p_s*T_r*D floats).  The second half is the caller's NCCL
+ * all_to_all_single (P:250 baseline: embedding kernels + RCCL All-to-All). */
+int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                       int64_t num_indices, void* stream, float* send);
+
+/* Cross-rank device barrier on `stream` (collective; benchmark tooling, not part of the op):
+ * returns immediately on the host; the stream proceeds once every rank's barrier kernel has
+ * arrived (system-scope release/acquire counters in the symmetric region).  Used to align the
+ * start of timed regions across GPUs.  Timeout -> ETIMEOUT on the next call. */
+int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
+
+/* Tunables (not collective, but keep them identical on all ranks; "slice" must be):
+ *   "slice"        S, pooled vectors per slice, >= 1 (P:147 user parameter; default 32)
+ *   "order"        0 comm-aware staggered (default), 1 comm-aware ascending, 2 oblivious
+ *                  (set before register_tables)
+ *   "chunk"        bags per work ticket, 1..63 (default 8; the largest divisor of S not above
+ *                  it is used): load-balance granularity, independent of the signal slice S
+ *                  (set before register_tables)
+ *   "threads"      consumer threads per CTA, multiple of 32 in [32, 256] (default 256); each
+ *                  CTA also has one producer warp
+ *   "minb"         register budget: 2 (<= 128 regs/thread) or 4 (<= 64 regs/thread) CTAs/SM
+ *   "timeout_ms"   receive-wait timeout (default 10000)
+ *   "validate"     1 = check indices/offsets on device before each forward (sync)
+ *   "unroll"       rows in flight per lane group: 0 = auto, else 2, 4, 8, 16
+ *   "stages"       shared-memory pipeline depth per CTA, 2..8 (default 4)
+ *   "ctas_per_sm"  persistent grid size per SM: 0 = max occupancy (P:280 occupancy study)
+ *   "idx_cap"      indices per pipeline stage (default 2048); a slice whose bags need more is
+ *                  split over several stages, and a single bag longer than this reads its
+ *                  indices from global memory
+ *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
+ *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
+ *   "debug_delay_ns"  test knob: CTAs sleep this long before signalling (stress tests)
+ *   "debug_skip_signal_to"  test knob: never signal rank v (>= 0), to exercise ETIMEOUT */
+int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t value);
+int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* value);
+
+/* Read-only facts about the current registration:
+ *   "rank", "world_size", "device", "epoch" (forwards issued), "local_batch" (b_r),
+ *   "total_tables" (G), "table_offset" (toff_r), "dim", "global_batch", "num_slices",
+ *   "num_chunks", "chunk_bags" (C),
+ *   "expected_in:<src>" (signals rank src sends here per forward), "region_bytes",
+ *   "last_grid" (CTAs of the last fused launch), "kernel_launches" (total kernels launched). */
+int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* value);
+
+/* Introspection for parity tests (synchronous; not on the hot path):
+ *  slice_plan:  decode every slice ticket ON THE DEVICE (the same decode the fused kernel uses)
+ *               into host out[n][4] = (dst s, local table t, first local row i0, rows nb).
+ *  read_flags:  host out[W] = this rank's arrival counters, one per source rank. */
+int emb_a2a_slice_plan(emb_a2a_t* h, int32_t* out, int64_t capacity, int64_t* n);
+int emb_a2a_read_flags(emb_a2a_t* h, uint64_t* out, int capacity);
+/* Trace log (set_option "trace" > 0): synchronises the device, copies the n records logged since
+ * the last read into host out[n][2] = {cta << 40 | event << 32 | payload, globaltimer_ns}, and
+ * restarts the log.  Events: 0 CTA start, 1 chunk ticket, 2 stage ready, 3 stage released
+ * (payload 1 = completed a remote slice and signalled it), 4 consumers done, 5 receive wait done. */
+int emb_a2a_read_trace(emb_a2a_t* h, uint64_t* out, int64_t capacity, int64_t* n);
+
+/* Collective teardown: synchronises the device, barriers through the all-gather so no peer is
+ * still writing, unmaps peers, frees the region.  h is invalid afterwards. */
+int emb_a2a_destroy(emb_a2a_t* h);
+
+const char* emb_a2a_last_error(const emb_a2a_t* h);
+const char* emb_a2a_status_string(int status);
+int emb_a2a_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMB_A2A_H_ */

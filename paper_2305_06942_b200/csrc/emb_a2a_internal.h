@@ -1,0 +1,113 @@
+// emb_a2a_internal.h -- shared between host.cpp (C ABI) and kernels.cu (sm_100a kernels).
+// Not installed; the public ABI is include/emb_a2a.h.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/emb_a2a.h"
+
+namespace emba2a {
+
+constexpr int kMaxW = EMB_A2A_MAX_WORLD;
+// Per-source arrival counters are padded to 128 B so concurrent writers never share a line.
+constexpr int kFlagStride = 16;  // uint64 words
+constexpr int kMaxStages = 8;    // shared-memory pipeline depth cap
+
+// Where peer s's receive buffers and our counter inside peer s's region live.  Device-resident,
+// written once per registration (the roc_shmem_ptr table of).
+struct DevPeers {
+  float* recv[kMaxW][2];                  // recv_s[parity] base, [b_s][G*D] float32
+  unsigned long long* flag_out[kMaxW];    // &flags_s[r]: counter r increments in peer s
+  long long n_in[kMaxW];                  // signals expected from source q per forward
+  unsigned long long* barrier_out[kMaxW]; // peer q's barrier counter (device barrier)
+};
+
+// Kernel parameters, passed by value (constant bank).  Scalars + the two small tables the
+// slice decode needs; everything per-peer is in DevPeers.
+struct KParams {
+  const int* indices;
+  const int* offsets;
+  const float* const* tables;   // device array of T pointers
+  float* send;                  // pool_local staging base ([B][T][D] by global row)
+  const DevPeers* peers;
+  unsigned long long* flags_in; // own counters, index src * kFlagStride
+  unsigned int* done;           // CTA completion counter (last-CTA detection)
+  unsigned int* ticket;         // next chunk ticket (beyond the first gridDim.x)
+  unsigned long long* slice_cnt;// per-slice completed-bag counters (monotone over epochs)
+  int* err;                     // device alias of the mapped host error word
+  unsigned long long* trace;    // optional %globaltimer event log (NULL = off); [0] = count
+  long long trace_cap;          // records (2 words each) after the header
+  long long B;
+  unsigned long long epoch;     // 1-based forward number
+  long long timeout_ns;
+  long long delay_ns;
+  int W, r, T, D4, G, toff, S, C, order, nslices, nchunks, idx_cap, nstages, stage_bytes,
+      skip_to, parity;
+  long long part[kMaxW + 1];    // batch partition prefix
+  int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
+  int chunk_base[kMaxW + 1];    // first chunk of destination ordinal k; [W] = nchunks
+};
+
+// Destination rank of ordinal k in rank r's slice order (row a1; R#19).
+__host__ __device__ inline int dest_of_ordinal(int order, int r, int W, int k) {
+  if (order == 0) return (k < W - 1) ? (r + 1 + k) % W : r;        // staggered remote, local last
+  if (order == 1) return (k < W - 1) ? (k < r ? k : k + 1) : r;    // ascending remote, local last
+  return k;                                                        // oblivious
+}
+
+// Work units of one rank, in issue order (row a1): for destination ordinal k = 0..W-1 (dest
+// s = dest_of_ordinal(k)), local table t, then row blocks of `unit` bags of s's batch block.
+// With unit = S these are the slices (signal granularity); with unit = C (C | S) they are
+// the chunks handed out as tickets (load-balance granularity).  base[k] = first unit of ordinal k.
+__host__ __device__ inline void decode_unit(const KParams& P, int ticket, int unit,
+                                            const int* base, int& k, int& s, int& t, int& i0,
+                                            int& nb) {
+  k = 0;
+  while (k < P.W - 1 && ticket >= base[k + 1]) ++k;
+  s = dest_of_ordinal(P.order, P.r, P.W, k);
+  const int q = ticket - base[k];
+  const long long b_s = P.part[s + 1] - P.part[s];
+  const int nu = (int)((b_s + unit - 1) / unit);
+  t = q / nu;
+  const int c = q - t * nu;
+  i0 = c * unit;
+  const long long rem = b_s - i0;
+  nb = rem < unit ? (int)rem : unit;
+}
+
+__host__ __device__ inline void decode_slice(const KParams& P, int ticket, int& s, int& t,
+                                             int& i0, int& nb) {
+  int k;
+  decode_unit(P, ticket, P.S, P.slice_base, k, s, t, i0, nb);
+}
+
+// Global slice id and size of the slice containing chunk (k, s, t, i0).
+__host__ __device__ inline void slice_of_chunk(const KParams& P, int k, int s, int t, int i0,
+                                               int& slice_id, int& slice_bags) {
+  const long long b_s = P.part[s + 1] - P.part[s];
+  const int nsl = (int)((b_s + P.S - 1) / P.S);
+  const int c = i0 / P.S;
+  slice_id = P.slice_base[k] + t * nsl + c;
+  const long long rem = b_s - (long long)c * P.S;
+  slice_bags = rem < P.S ? (int)rem : P.S;
+}
+
+struct LaunchCfg {
+  int threads;      // consumer threads per CTA (+1 producer warp)
+  int unroll;       // 0 auto
+  int ctas_per_sm;  // persistent grid: 0 = max occupancy
+  int minb;         // register budget: 2 (<=128 regs) or 4 (<=64 regs) CTAs of 256 per SM
+};
+
+// Launchers (kernels.cu).  Return cudaError_t of the launch.
+cudaError_t launch_fused(const KParams& P, const LaunchCfg& c, cudaStream_t st, int* grid_out);
+cudaError_t launch_pool_local(const KParams& P, const LaunchCfg& c, cudaStream_t st);
+cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,
+                           unsigned long long target, long long timeout_ns, int* err,
+                           cudaStream_t st);
+cudaError_t launch_slice_plan(const KParams& P, int* out, cudaStream_t st);
+cudaError_t launch_validate(const int* indices, const int* offsets, long long nnz, long long TB,
+                            long long B, int T, const long long* rows_dev, int* err_dev,
+                            cudaStream_t st);
+
+}  // namespace emba2a

@@ -1,0 +1,820 @@
+// host.cpp -- the C ABI of libemba2a.so (include/emb_a2a.h).
+//
+// Owns: the symmetric receive region ("symmetric heap"; here a library-owned cudaMalloc
+// exported with cudaIpcGetMemHandle), the peer pointer table (roc_shmem_ptr analogue),
+// epochs, validation and error state.  Every step of the forward runs in kernels.cu.
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "emb_a2a_internal.h"
+
+using namespace emba2a;
+
+namespace {
+
+constexpr uint32_t kMagic = 0xE2BA2A01u;
+
+struct Meta {           // phase-1 all-gather record (problem statement)
+  uint32_t magic, abi;
+  int32_t rank, world, T, D;
+  int64_t B;
+  int64_t part[kMaxW + 1];
+  int32_t S, pad;
+};
+
+struct Handles {        // phase-2 all-gather record (symmetric region)
+  uint32_t magic;
+  int32_t pid;
+  int32_t device;
+  int32_t pad;
+  uint64_t host_id;
+  uint64_t raw_ptr;
+  uint64_t region_bytes;
+  cudaIpcMemHandle_t ipc;
+};
+
+uint64_t host_id() {
+  char name[256] = {0};
+  gethostname(name, sizeof(name) - 1);
+  uint64_t h = 1469598103934665603ull;
+  for (const char* p = name; *p; ++p) h = (h ^ (uint8_t)*p) * 1099511628211ull;
+  return h;
+}
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (prev_ != dev) cudaSetDevice(dev);
+    dev_ = dev;
+  }
+  ~DeviceGuard() {
+    if (prev_ != dev_) cudaSetDevice(prev_);
+  }
+ private:
+  int prev_ = 0, dev_ = 0;
+};
+
+}  // namespace
+
+struct emb_a2a {
+  int rank = 0, W = 1, dev = 0;
+  emb_a2a_allgather_fn allgather = nullptr;
+  void* user = nullptr;
+  bool registered = false, poisoned = false;
+  std::string last_error;
+
+  // problem
+  int T = 0, D = 0, G = 0, toff = 0;
+  int64_t B = 0, b = 0;
+  std::vector<int64_t> part;
+  std::vector<int32_t> allT;
+  std::vector<int64_t> rows;
+
+  // options
+  int64_t S = 32, order = 0, threads = 256, timeout_ms = 10000, validate = 0, unroll = 0;
+  int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, minb = 2;
+  int64_t chunk = 8;
+  int64_t trace_cap = 0;                 // records; 0 = tracing off
+  unsigned long long* d_trace = nullptr;
+
+  // device state
+  char* region = nullptr;
+  size_t region_bytes = 0;
+  unsigned long long* flags = nullptr;   // own counters
+  float* recv[2] = {nullptr, nullptr};
+  std::vector<void*> opened;             // IPC-opened peer bases
+  DevPeers host_peers{};
+  DevPeers* d_peers = nullptr;
+  const float** d_tables = nullptr;
+  long long* d_rows = nullptr;
+  unsigned int* d_done = nullptr;        // [fused done, fused ticket, pool done, pool ticket]
+  unsigned long long* d_slice_cnt = nullptr;   // per-slice completed-bag counters
+  int* h_err = nullptr;                  // mapped pinned host
+  int* d_err = nullptr;
+  int* h_verr = nullptr;                 // validate error word (mapped)
+  int* d_verr = nullptr;
+  int32_t* d_idx_stage = nullptr;
+  int32_t* d_off_stage = nullptr;
+  size_t idx_stage_cap = 0, off_stage_cap = 0;
+
+  uint64_t epoch = 0;
+  uint64_t barrier_epoch = 0;
+  int nslices = 0;
+  int slice_base[kMaxW + 1] = {0};
+  int chunk_base[kMaxW + 1] = {0};
+  int C = 8, nchunks = 0;
+  int last_grid = 0;
+  int64_t kernel_launches = 0;
+};
+
+namespace {
+
+int fail(emb_a2a* h, int code, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    h->last_error = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(h, call)                                                                 \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail((h), e_ == cudaErrorMemoryAllocation ? EMB_A2A_ENOMEM : EMB_A2A_ECUDA,  \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);   \
+    }                                                                                     \
+  } while (0)
+
+// Poll the asynchronous error word; poison the handle on failure.
+int check_async(emb_a2a* h) {
+  if (h->poisoned) return fail(h, EMB_A2A_ESTATE, "handle poisoned by an earlier failure: %s",
+                               h->last_error.c_str());
+  if (h->h_err && *(volatile int*)h->h_err != 0) {
+    const int v = *(volatile int*)h->h_err;
+    h->poisoned = true;
+    return fail(h, EMB_A2A_ETIMEOUT,
+                (v & 0x200) ? "device barrier timed out on rank %d (code %d, timeout_ms=%lld)"
+                            : "receive wait timed out: rank %d never received all slices from "
+                              "rank %d (timeout_ms=%lld)",
+                h->rank, v & 0xff, (long long)h->timeout_ms);
+  }
+  return EMB_A2A_OK;
+}
+
+void release_registration(emb_a2a* h) {
+  for (void* p : h->opened) cudaIpcCloseMemHandle(p);
+  h->opened.clear();
+  if (h->region) cudaFree(h->region);
+  if (h->d_peers) cudaFree(h->d_peers);
+  if (h->d_tables) cudaFree(h->d_tables);
+  if (h->d_rows) cudaFree(h->d_rows);
+  if (h->d_done) cudaFree(h->d_done);
+  if (h->d_slice_cnt) cudaFree(h->d_slice_cnt);
+  if (h->d_trace) cudaFree(h->d_trace);
+  h->d_trace = nullptr;
+  h->d_slice_cnt = nullptr;
+  if (h->d_idx_stage) cudaFree(h->d_idx_stage);
+  if (h->d_off_stage) cudaFree(h->d_off_stage);
+  h->region = nullptr;
+  h->d_peers = nullptr;
+  h->d_tables = nullptr;
+  h->d_rows = nullptr;
+  h->d_done = nullptr;
+  h->d_idx_stage = nullptr;
+  h->d_off_stage = nullptr;
+  h->idx_stage_cap = h->off_stage_cap = 0;
+  h->flags = nullptr;
+  h->recv[0] = h->recv[1] = nullptr;
+  h->registered = false;
+}
+
+int barrier(emb_a2a* h) {
+  std::vector<char> recv(h->W);
+  char one = 1;
+  if (h->allgather(&one, recv.data(), 1, h->user) != 0)
+    return fail(h, EMB_A2A_EBOOT, "all-gather callback failed (barrier)");
+  return EMB_A2A_OK;
+}
+
+// Chunk size: the largest divisor of S that is <= the "chunk" option (and <= 63, the producer
+// keeps a chunk's offsets in two registers per lane).
+int chunk_size(int64_t S, int64_t want) {
+  int64_t c = std::min<int64_t>(std::min<int64_t>(want, S), 63);
+  while (c > 1 && S % c != 0) --c;
+  return (int)std::max<int64_t>(c, 1);
+}
+
+// Slice and chunk counts per destination ordinal (row a1): T * ceil(b_s / unit).
+void compute_slices(emb_a2a* h) {
+  h->C = chunk_size(h->S, h->chunk);
+  int64_t acc = 0, accc = 0;
+  for (int k = 0; k < h->W; ++k) {
+    h->slice_base[k] = (int)acc;
+    h->chunk_base[k] = (int)accc;
+    const int s = dest_of_ordinal((int)h->order, h->rank, h->W, k);
+    const int64_t bs = h->part[s + 1] - h->part[s];
+    acc += (int64_t)h->T * ((bs + h->S - 1) / h->S);
+    accc += (int64_t)h->T * ((bs + h->C - 1) / h->C);
+  }
+  h->slice_base[h->W] = (int)acc;
+  h->chunk_base[h->W] = (int)accc;
+  h->nslices = (int)acc;
+  h->nchunks = (int)accc;
+  for (int q = 0; q < h->W; ++q) {
+    const int64_t nsl = (h->b + h->S - 1) / h->S;
+    h->host_peers.n_in[q] = (q == h->rank) ? 0 : (long long)h->allT[q] * nsl;
+  }
+}
+
+KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) {
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.indices = indices;
+  P.offsets = offsets;
+  P.tables = h->d_tables;
+  P.peers = h->d_peers;
+  P.flags_in = h->flags;
+  P.done = h->d_done;
+  P.ticket = h->d_done + 1;
+  P.err = h->d_err;
+  P.trace = h->d_trace;
+  P.trace_cap = h->trace_cap;
+  P.B = h->B;
+  P.epoch = h->epoch;
+  P.timeout_ns = (long long)h->timeout_ms * 1000000ll;
+  P.delay_ns = h->delay_ns;
+  P.W = h->W;
+  P.r = h->rank;
+  P.T = h->T;
+  P.D4 = h->D / 4;
+  P.G = h->G;
+  P.toff = h->toff;
+  P.S = (int)h->S;
+  P.order = (int)h->order;
+  P.nslices = h->nslices;
+  P.idx_cap = (int)h->idx_cap;
+  P.C = h->C;
+  P.nchunks = h->nchunks;
+  P.slice_cnt = h->d_slice_cnt;
+  P.nstages = (int)h->stages;
+  P.skip_to = (int)h->skip_to;
+  P.parity = (int)(h->epoch & 1);
+  for (int s = 0; s <= h->W; ++s) {
+    P.part[s] = h->part[s];
+    P.slice_base[s] = h->slice_base[s];
+    P.chunk_base[s] = h->chunk_base[s];
+  }
+  return P;
+}
+
+int push_peers(emb_a2a* h) {
+  CUDA_TRY(h, cudaMemcpy(h->d_peers, &h->host_peers, sizeof(DevPeers), cudaMemcpyHostToDevice));
+  return EMB_A2A_OK;
+}
+
+int run_validate(emb_a2a* h, const int32_t* indices, const int32_t* offsets, int64_t nnz,
+                 cudaStream_t st) {
+  *(volatile int*)h->h_verr = 0;
+  CUDA_TRY(h, launch_validate(indices, offsets, nnz, (long long)h->T * h->B, h->B, h->T,
+                              h->d_rows, h->d_verr, st));
+  h->kernel_launches++;
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  const int v = *(volatile int*)h->h_verr;
+  if (v) return fail(h, EMB_A2A_EINDEX, v == 1 ? "malformed offsets" : "index out of range");
+  return EMB_A2A_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int emb_a2a_abi_version(void) { return EMB_A2A_ABI_VERSION; }
+
+const char* emb_a2a_status_string(int s) {
+  switch (s) {
+    case EMB_A2A_OK: return "EMB_A2A_OK";
+    case EMB_A2A_EINVAL: return "EMB_A2A_EINVAL";
+    case EMB_A2A_ESTATE: return "EMB_A2A_ESTATE";
+    case EMB_A2A_ECUDA: return "EMB_A2A_ECUDA";
+    case EMB_A2A_ENOMEM: return "EMB_A2A_ENOMEM";
+    case EMB_A2A_EPEER: return "EMB_A2A_EPEER";
+    case EMB_A2A_EBOOT: return "EMB_A2A_EBOOT";
+    case EMB_A2A_ETIMEOUT: return "EMB_A2A_ETIMEOUT";
+    case EMB_A2A_EINDEX: return "EMB_A2A_EINDEX";
+    default: return "EMB_A2A_UNKNOWN";
+  }
+}
+
+const char* emb_a2a_last_error(const emb_a2a_t* h) {
+  return h ? h->last_error.c_str() : "null handle";
+}
+
+int emb_a2a_init(int rank, int world_size, int cuda_device, emb_a2a_allgather_fn allgather,
+                 void* user, emb_a2a_t** out) {
+  if (!out) return EMB_A2A_EINVAL;
+  *out = nullptr;
+  if (world_size < 1 || world_size > kMaxW || rank < 0 || rank >= world_size || !allgather)
+    return EMB_A2A_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+    return EMB_A2A_ECUDA;
+  emb_a2a* h = new emb_a2a();
+  h->rank = rank;
+  h->W = world_size;
+  h->dev = cuda_device;
+  h->allgather = allgather;
+  h->user = user;
+  DeviceGuard g(cuda_device);
+  cudaError_t e = cudaHostAlloc((void**)&h->h_err, 2 * sizeof(int), cudaHostAllocMapped);
+  if (e != cudaSuccess) {
+    delete h;
+    return EMB_A2A_ENOMEM;
+  }
+  h->h_err[0] = h->h_err[1] = 0;
+  h->h_verr = h->h_err + 1;
+  if (cudaHostGetDevicePointer((void**)&h->d_err, h->h_err, 0) != cudaSuccess) {
+    cudaFreeHost(h->h_err);
+    delete h;
+    return EMB_A2A_ECUDA;
+  }
+  h->d_verr = h->d_err + 1;
+  *out = h;
+  return EMB_A2A_OK;
+}
+
+static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const* tables,
+                         const int64_t* rows, int dim, int64_t global_batch,
+                         const int64_t* batch_partition);
+
+int emb_a2a_register_tables(emb_a2a_t* h, int num_local_tables, const float* const* tables,
+                            const int64_t* rows, int dim, int64_t global_batch,
+                            const int64_t* batch_partition) {
+  if (!h) return EMB_A2A_EINVAL;
+  const int rc = register_impl(h, num_local_tables, tables, rows, dim, global_batch,
+                               batch_partition);
+  if (rc != EMB_A2A_OK && !h->registered) {
+    DeviceGuard guard(h->dev);
+    release_registration(h);
+  }
+  return rc;
+}
+
+static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const* tables,
+                         const int64_t* rows, int dim, int64_t global_batch,
+                         const int64_t* batch_partition) {
+  if (h->poisoned) return check_async(h);
+  DeviceGuard guard(h->dev);
+  if (h->registered) {   // collective re-registration: quiesce, barrier, tear down
+    cudaDeviceSynchronize();
+    int rc = barrier(h);
+    if (rc) return rc;
+    release_registration(h);
+  }
+  // ---- local validation (identical decisions on every rank would be ideal; metadata
+  //      mismatches are caught after the all-gather so every rank returns EINVAL together)
+  int bad = 0;
+  if (num_local_tables < 0 || (num_local_tables > 0 && (!tables || !rows))) bad = 1;
+  if (dim < 4 || dim > 1024 || dim % 4 != 0) bad = 1;
+  if (global_batch < 0) bad = 1;
+  for (int t = 0; !bad && t < num_local_tables; ++t) {
+    if (rows[t] < 1 || rows[t] >= (1ll << 31)) bad = 1;
+    if (((uintptr_t)tables[t]) % 16 != 0 || !tables[t]) bad = 1;
+  }
+  Meta me;
+  memset(&me, 0, sizeof(me));
+  me.magic = kMagic;
+  me.abi = EMB_A2A_ABI_VERSION;
+  me.rank = h->rank;
+  me.world = h->W;
+  me.T = num_local_tables;
+  me.D = dim;
+  me.B = global_batch;
+  me.S = (int32_t)h->S;
+  if (batch_partition) {
+    for (int s = 0; s <= h->W; ++s) me.part[s] = batch_partition[s];
+  } else if (h->W > 0 && global_batch % h->W == 0) {
+    for (int s = 0; s <= h->W; ++s) me.part[s] = global_batch / h->W * s;
+  } else {
+    bad = 1;
+  }
+  if (me.part[0] != 0 || me.part[h->W] != global_batch) bad = 1;
+  for (int s = 0; s < h->W; ++s)
+    if (me.part[s + 1] < me.part[s]) bad = 1;
+  if (bad) me.magic = 0;   // tell everyone
+
+  std::vector<Meta> all(h->W);
+  if (h->allgather(&me, all.data(), sizeof(Meta), h->user) != 0)
+    return fail(h, EMB_A2A_EBOOT, "all-gather callback failed (metadata)");
+  int64_t G = 0;
+  for (int q = 0; q < h->W; ++q) {
+    const Meta& m = all[q];
+    if (m.magic != kMagic || m.abi != EMB_A2A_ABI_VERSION || m.rank != q || m.world != h->W)
+      return fail(h, EMB_A2A_EINVAL, "rank %d sent invalid registration arguments", q);
+    if (m.D != dim || m.B != global_batch || m.S != (int32_t)h->S ||
+        memcmp(m.part, me.part, sizeof(int64_t) * (h->W + 1)) != 0)
+      return fail(h, EMB_A2A_EINVAL,
+                  "ranks disagree on dim / global batch / partition / slice (rank %d)", q);
+    G += m.T;
+  }
+  if (G < 1) return fail(h, EMB_A2A_EINVAL, "no tables registered on any rank");
+  int64_t nnz_tb = (int64_t)num_local_tables * global_batch;
+  if (nnz_tb + 1 >= (1ll << 31) || G * (int64_t)dim >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "T*B or G*D too large for int32 CSR / layout (R#8)");
+
+  h->T = num_local_tables;
+  h->D = dim;
+  h->B = global_batch;
+  h->G = (int)G;
+  h->part.assign(me.part, me.part + h->W + 1);
+  h->b = h->part[h->rank + 1] - h->part[h->rank];
+  h->allT.resize(h->W);
+  h->toff = 0;
+  for (int q = 0; q < h->W; ++q) {
+    h->allT[q] = all[q].T;
+    if (q < h->rank) h->toff += all[q].T;
+  }
+  h->rows.assign(rows, rows + num_local_tables);
+
+  // ---- symmetric region: [arrival counters W x 128 B | barrier counter 128 B | recv0 | recv1],
+  //      256-B aligned pieces
+  const size_t flag_bytes = ((size_t)(h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
+  const size_t buf_bytes = ((size_t)h->b * G * dim * 4 + 255) / 256 * 256;
+  h->region_bytes = flag_bytes + 2 * std::max<size_t>(buf_bytes, 256);
+  CUDA_TRY(h, cudaMalloc((void**)&h->region, h->region_bytes));
+  CUDA_TRY(h, cudaMemset(h->region, 0, h->region_bytes));
+  h->flags = (unsigned long long*)h->region;
+  h->recv[0] = (float*)(h->region + flag_bytes);
+  h->recv[1] = (float*)(h->region + flag_bytes + std::max<size_t>(buf_bytes, 256));
+
+  Handles mine;
+  memset(&mine, 0, sizeof(mine));
+  mine.magic = kMagic;
+  mine.pid = (int32_t)getpid();
+  mine.device = h->dev;
+  mine.host_id = host_id();
+  mine.raw_ptr = (uint64_t)(uintptr_t)h->region;
+  mine.region_bytes = h->region_bytes;
+  CUDA_TRY(h, cudaIpcGetMemHandle(&mine.ipc, h->region));
+  std::vector<Handles> hs(h->W);
+  if (h->allgather(&mine, hs.data(), sizeof(Handles), h->user) != 0)
+    return fail(h, EMB_A2A_EBOOT, "all-gather callback failed (handles)");
+
+  // ---- map every peer (roc_shmem_ptr gives the peer's virtual address)
+  memset(&h->host_peers, 0, sizeof(DevPeers));
+  for (int q = 0; q < h->W; ++q) {
+    char* base = nullptr;
+    const Handles& o = hs[q];
+    if (q == h->rank) {
+      base = h->region;
+    } else if (o.pid == mine.pid && o.host_id == mine.host_id) {
+      base = (char*)(uintptr_t)o.raw_ptr;     // same process: raw pointer (loopback / threads)
+      if (o.device != h->dev) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, h->dev, o.device);
+        if (!can) return fail(h, EMB_A2A_EPEER, "no P2P path from device %d to %d", h->dev,
+                              o.device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(o.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(h, EMB_A2A_EPEER, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+    } else {
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, o.ipc, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        return fail(h, EMB_A2A_EPEER, "cudaIpcOpenMemHandle(rank %d): %s", q,
+                    cudaGetErrorString(e));
+      h->opened.push_back(p);
+      base = (char*)p;
+    }
+    const int64_t bq = h->part[q + 1] - h->part[q];
+    const size_t fq = flag_bytes;   // identical layout on every rank (same W)
+    const size_t bufq = std::max<size_t>(((size_t)bq * G * dim * 4 + 255) / 256 * 256, 256);
+    h->host_peers.recv[q][0] = (float*)(base + fq);
+    h->host_peers.recv[q][1] = (float*)(base + fq + bufq);
+    h->host_peers.flag_out[q] = (unsigned long long*)(base) + (size_t)h->rank * kFlagStride;
+    h->host_peers.barrier_out[q] = (unsigned long long*)(base) + (size_t)h->W * kFlagStride;
+  }
+
+  // ---- device-side tables, plan, counters
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_peers, sizeof(DevPeers)));
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_tables, sizeof(float*) * std::max(1, h->T)));
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_rows, sizeof(long long) * std::max(1, h->T)));
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_done, 4 * sizeof(unsigned int)));
+  CUDA_TRY(h, cudaMemset(h->d_done, 0, 4 * sizeof(unsigned int)));
+  if (h->T > 0) {
+    CUDA_TRY(h, cudaMemcpy(h->d_tables, tables, sizeof(float*) * h->T, cudaMemcpyHostToDevice));
+    std::vector<long long> r64(rows, rows + h->T);
+    CUDA_TRY(h, cudaMemcpy(h->d_rows, r64.data(), sizeof(long long) * h->T,
+                           cudaMemcpyHostToDevice));
+  }
+  compute_slices(h);
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_slice_cnt, sizeof(unsigned long long) *
+                                                      std::max(1, h->nslices)));
+  CUDA_TRY(h, cudaMemset(h->d_slice_cnt, 0, sizeof(unsigned long long) *
+                                               std::max(1, h->nslices)));
+  int rc = push_peers(h);
+  if (rc) return rc;
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  h->epoch = 0;
+  h->barrier_epoch = 0;
+  h->registered = true;
+  return barrier(h);   // nobody forwards before everyone has mapped everyone
+}
+
+int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                    int64_t num_indices, void* stream, float** out, int64_t* out_rows,
+                    int64_t* out_cols) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "forward before register_tables");
+  if (!out) return fail(h, EMB_A2A_EINVAL, "out is NULL");
+  if (num_indices < 0 || num_indices >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "num_indices out of range (int32 CSR, R#8)");
+  if ((h->T > 0 && h->B > 0) && (!offsets || (num_indices > 0 && !indices)))
+    return fail(h, EMB_A2A_EINVAL, "indices/offsets are NULL");
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->validate && h->T > 0 && h->B > 0) {
+    rc = run_validate(h, indices, offsets, num_indices, st);
+    if (rc) return rc;
+  }
+  h->epoch += 1;
+  KParams P = make_params(h, indices, offsets);
+  LaunchCfg c{(int)h->threads, (int)h->unroll, (int)h->ctas_per_sm, (int)h->minb};
+  cudaError_t e = launch_fused(P, c, st, &h->last_grid);
+  if (e != cudaSuccess) {
+    h->poisoned = true;
+    return fail(h, EMB_A2A_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+  }
+  h->kernel_launches++;
+  *out = h->recv[h->epoch & 1];
+  if (out_rows) *out_rows = h->b;
+  if (out_cols) *out_cols = (int64_t)h->G * h->D;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
+                         int64_t num_indices, void* stream, float* h_out) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "forward_host before register_tables");
+  if (num_indices < 0 || num_indices >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "num_indices out of range");
+  if (!h_out || (!h_offsets && h->T > 0 && h->B > 0) || (num_indices > 0 && !h_indices))
+    return fail(h, EMB_A2A_EINVAL, "host buffers are NULL");
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nidx = (size_t)std::max<int64_t>(num_indices, 1);
+  const size_t noff = (size_t)h->T * h->B + 1;
+  if (nidx > h->idx_stage_cap) {
+    if (h->d_idx_stage) cudaFree(h->d_idx_stage);
+    h->d_idx_stage = nullptr;
+    h->idx_stage_cap = 0;
+    CUDA_TRY(h, cudaMalloc((void**)&h->d_idx_stage, nidx * sizeof(int32_t)));
+    h->idx_stage_cap = nidx;
+  }
+  if (noff > h->off_stage_cap) {
+    if (h->d_off_stage) cudaFree(h->d_off_stage);
+    h->d_off_stage = nullptr;
+    h->off_stage_cap = 0;
+    CUDA_TRY(h, cudaMalloc((void**)&h->d_off_stage, noff * sizeof(int32_t)));
+    h->off_stage_cap = noff;
+  }
+  if (num_indices > 0)
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_idx_stage, h_indices, num_indices * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+  if (h->T > 0 && h->B > 0)
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_off_stage, h_offsets, noff * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+  float* dout = nullptr;
+  rc = emb_a2a_forward(h, h->d_idx_stage, h->d_off_stage, num_indices, stream, &dout, nullptr,
+                       nullptr);
+  if (rc) return rc;
+  const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
+  if (out_bytes) CUDA_TRY(h, cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                       int64_t num_indices, void* stream, float* send) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "pool_local before register_tables");
+  if (num_indices < 0 || num_indices >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "num_indices out of range");
+  if (h->T > 0 && h->B > 0 && (!send || !offsets || (num_indices > 0 && !indices)))
+    return fail(h, EMB_A2A_EINVAL, "NULL buffer");
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->validate && h->T > 0 && h->B > 0) {
+    rc = run_validate(h, indices, offsets, num_indices, st);
+    if (rc) return rc;
+  }
+  KParams P = make_params(h, indices, offsets);
+  P.send = send;
+  P.done = h->d_done + 2;      // own counters: may run concurrently with a forward's kernel
+  P.ticket = h->d_done + 3;
+  LaunchCfg c{(int)h->threads, (int)h->unroll, (int)h->ctas_per_sm, (int)h->minb};
+  cudaError_t e = launch_pool_local(P, c, st);
+  if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "pool kernel launch: %s",
+                                    cudaGetErrorString(e));
+  if (P.nslices > 0) h->kernel_launches++;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "device_barrier before register_tables");
+  if (h->W == 1) return EMB_A2A_OK;
+  DeviceGuard guard(h->dev);
+  h->barrier_epoch += 1;
+  CUDA_TRY(h, launch_barrier(h->d_peers, h->flags + (size_t)h->W * kFlagStride, h->W, h->rank,
+                             h->barrier_epoch * (unsigned long long)(h->W - 1),
+                             (long long)h->timeout_ms * 1000000ll, h->d_err,
+                             (cudaStream_t)stream));
+  h->kernel_launches++;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
+  if (!h || !key) return EMB_A2A_EINVAL;
+  std::string k(key);
+  if (k == "slice") {
+    if (v < 1 || v > (1 << 20)) return fail(h, EMB_A2A_EINVAL, "slice must be in [1, 2^20]");
+    if (h->registered && v != h->S) {
+      // counters are monotone per (epoch x expected count): changing S mid-stream would break
+      // the epoch arithmetic, so it is only allowed before register_tables.
+      return fail(h, EMB_A2A_ESTATE, "set 'slice' before register_tables");
+    }
+    h->S = v;
+  } else if (k == "order") {
+    if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "order must be 0, 1 or 2");
+    if (h->registered && v != h->order)   // slice ids (and their counters) depend on the order
+      return fail(h, EMB_A2A_ESTATE, "set 'order' before register_tables");
+    h->order = v;
+  } else if (k == "chunk") {
+    if (v < 1 || v > 63) return fail(h, EMB_A2A_EINVAL, "chunk in [1, 63]");
+    if (h->registered && v != h->chunk)
+      return fail(h, EMB_A2A_ESTATE, "set 'chunk' before register_tables");
+    h->chunk = v;
+  } else if (k == "threads") {
+    if (v < 32 || v > 256 || v % 32) return fail(h, EMB_A2A_EINVAL, "threads: 32..256, x32");
+    h->threads = v;
+  } else if (k == "timeout_ms") {
+    if (v < 1) return fail(h, EMB_A2A_EINVAL, "timeout_ms >= 1");
+    h->timeout_ms = v;
+  } else if (k == "validate") {
+    h->validate = v ? 1 : 0;
+  } else if (k == "unroll") {
+    if (!(v == 0 || v == 2 || v == 4 || v == 8 || v == 16))
+      return fail(h, EMB_A2A_EINVAL, "unroll in {0,2,4,8,16}");
+    h->unroll = v;
+  } else if (k == "idx_cap") {
+    if (v < 0 || v > 16384) return fail(h, EMB_A2A_EINVAL, "idx_cap in [0, 16384]");
+    h->idx_cap = v;
+  } else if (k == "minb") {
+    if (v != 2 && v != 4) return fail(h, EMB_A2A_EINVAL, "minb in {2, 4}");
+    h->minb = v;
+  } else if (k == "stages") {
+    if (v < 2 || v > kMaxStages) return fail(h, EMB_A2A_EINVAL, "stages in [2, %d]", kMaxStages);
+    h->stages = v;
+  } else if (k == "ctas_per_sm") {
+    if (v < 0 || v > 32) return fail(h, EMB_A2A_EINVAL, "ctas_per_sm in [0, 32]");
+    h->ctas_per_sm = v;
+  } else if (k == "trace") {
+    if (v < 0 || v > (1 << 24)) return fail(h, EMB_A2A_EINVAL, "trace records in [0, 2^24]");
+    DeviceGuard guard(h->dev);
+    if (h->d_trace) cudaFree(h->d_trace);
+    h->d_trace = nullptr;
+    h->trace_cap = 0;
+    if (v > 0) {
+      CUDA_TRY(h, cudaMalloc((void**)&h->d_trace, (size_t)(2 + 2 * v) * 8));
+      CUDA_TRY(h, cudaMemset(h->d_trace, 0, (size_t)(2 + 2 * v) * 8));
+      h->trace_cap = v;
+    }
+  } else if (k == "debug_delay_ns") {
+    h->delay_ns = std::max<int64_t>(0, v);
+  } else if (k == "debug_skip_signal_to") {
+    h->skip_to = v;
+  } else {
+    return fail(h, EMB_A2A_EINVAL, "unknown option '%s'", key);
+  }
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
+  if (!h || !key || !v) return EMB_A2A_EINVAL;
+  std::string k(key);
+  if (k == "slice") *v = h->S;
+  else if (k == "order") *v = h->order;
+  else if (k == "threads") *v = h->threads;
+  else if (k == "timeout_ms") *v = h->timeout_ms;
+  else if (k == "validate") *v = h->validate;
+  else if (k == "unroll") *v = h->unroll;
+  else if (k == "idx_cap") *v = h->idx_cap;
+  else if (k == "stages") *v = h->stages;
+  else if (k == "chunk") *v = h->chunk;
+  else if (k == "trace") *v = h->trace_cap;
+  else if (k == "minb") *v = h->minb;
+  else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
+  else if (k == "debug_delay_ns") *v = h->delay_ns;
+  else if (k == "debug_skip_signal_to") *v = h->skip_to;
+  else return EMB_A2A_EINVAL;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* v) {
+  if (!h || !key || !v) return EMB_A2A_EINVAL;
+  std::string k(key);
+  if (k == "rank") *v = h->rank;
+  else if (k == "world_size") *v = h->W;
+  else if (k == "device") *v = h->dev;
+  else if (k == "epoch") *v = (int64_t)h->epoch;
+  else if (k == "kernel_launches") *v = h->kernel_launches;
+  else if (!h->registered) return EMB_A2A_ESTATE;
+  else if (k == "local_batch") *v = h->b;
+  else if (k == "total_tables") *v = h->G;
+  else if (k == "local_tables") *v = h->T;
+  else if (k == "table_offset") *v = h->toff;
+  else if (k == "dim") *v = h->D;
+  else if (k == "global_batch") *v = h->B;
+  else if (k == "num_slices") *v = h->nslices;
+  else if (k == "num_chunks") *v = h->nchunks;
+  else if (k == "chunk_bags") *v = h->C;
+  else if (k == "region_bytes") *v = (int64_t)h->region_bytes;
+  else if (k == "last_grid") *v = h->last_grid;
+  else if (k.rfind("expected_in:", 0) == 0) {
+    const int q = atoi(k.c_str() + 12);
+    if (q < 0 || q >= h->W) return EMB_A2A_EINVAL;
+    *v = h->host_peers.n_in[q];
+  } else {
+    return EMB_A2A_EINVAL;
+  }
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_slice_plan(emb_a2a_t* h, int32_t* out, int64_t capacity, int64_t* n) {
+  if (!h || !n) return EMB_A2A_EINVAL;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "not registered");
+  *n = h->nslices;
+  if (capacity < h->nslices || (!out && h->nslices > 0))
+    return fail(h, EMB_A2A_EINVAL, "capacity %lld < %d slices", (long long)capacity,
+                h->nslices);
+  if (h->nslices == 0) return EMB_A2A_OK;
+  DeviceGuard guard(h->dev);
+  int* d = nullptr;
+  CUDA_TRY(h, cudaMalloc((void**)&d, sizeof(int) * 4 * h->nslices));
+  KParams P = make_params(h, nullptr, nullptr);
+  cudaError_t e = launch_slice_plan(P, d, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d, sizeof(int) * 4 * h->nslices,
+                                       cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "slice_plan: %s", cudaGetErrorString(e));
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_read_trace(emb_a2a_t* h, uint64_t* out, int64_t capacity, int64_t* n) {
+  if (!h || !n) return EMB_A2A_EINVAL;
+  if (!h->d_trace) return fail(h, EMB_A2A_ESTATE, "tracing is off (set_option trace)");
+  DeviceGuard guard(h->dev);
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  unsigned long long cnt = 0;
+  CUDA_TRY(h, cudaMemcpy(&cnt, h->d_trace, 8, cudaMemcpyDeviceToHost));
+  const int64_t m = std::min<int64_t>((int64_t)cnt, h->trace_cap);
+  *n = m;
+  if (capacity < m || (!out && m > 0)) return fail(h, EMB_A2A_EINVAL, "capacity < %lld", (long long)m);
+  if (m > 0) CUDA_TRY(h, cudaMemcpy(out, h->d_trace + 2, (size_t)m * 16, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemset(h->d_trace, 0, 8));   // restart the log
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_read_flags(emb_a2a_t* h, uint64_t* out, int capacity) {
+  if (!h || !out || capacity < h->W) return EMB_A2A_EINVAL;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "not registered");
+  DeviceGuard guard(h->dev);
+  std::vector<unsigned long long> buf((size_t)h->W * kFlagStride);
+  CUDA_TRY(h, cudaMemcpy(buf.data(), h->flags, buf.size() * 8, cudaMemcpyDeviceToHost));
+  for (int q = 0; q < h->W; ++q) out[q] = buf[(size_t)q * kFlagStride];
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_destroy(emb_a2a_t* h) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = EMB_A2A_OK;
+  {
+    DeviceGuard guard(h->dev);
+    if (h->registered) {
+      cudaDeviceSynchronize();
+      rc = barrier(h);                      // no peer is still writing into our region
+      for (void* p : h->opened) cudaIpcCloseMemHandle(p);
+      h->opened.clear();
+      int rc2 = barrier(h);                 // every peer has unmapped us
+      if (!rc) rc = rc2;
+      release_registration(h);
+    }
+    if (h->h_err) cudaFreeHost(h->h_err);
+  }
+  delete h;
+  return rc;
+}
+
+}  // extern "C"

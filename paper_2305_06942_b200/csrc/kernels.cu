@@ -1,0 +1,618 @@
+// kernels.cu -- sm_100a kernels of libemba2a.so.
+//
+// The fused kernel (rows a1-a8 of SURVEY.md Sec 8) performs, for one slice per CTA:
+//   a1  decode the CTA's ticket into a slice (dst s, local table t, rows [i0, i0+nb)) in
+//       comm-aware order: remote slices first, destinations staggered (R#19)
+//   a2  stage the slice's CSR offsets and (contiguous) indices in shared memory
+//   a3  gather table rows with 16-byte read-only vector loads, U rows in flight per lane group
+//   a4  sum-pool in fp32, ascending bag order, from +0.0 (R#5)
+//   a5  place: row i = j - p_s, columns (toff + t) * D of s's [b_s][G*D] buffer
+//   a6  store straight into the destination GPU's receive buffer (zero-copy)
+//   a7  after the CTA barrier, ONE thread releases the slice: red.release.sys.add on the
+//       per-source counter in the destination's memory (PUT -> fence -> sliceRdy)
+//   a8  the last CTA to finish polls the W-1 incoming counters with ld.acquire.sys until every
+//       peer's slices for this epoch have arrived ("poll ... before exiting")
+// The unfused baseline kernel (pool_local) runs the same gather body and stores to a local
+// dest-major staging buffer instead ("stored into an intermediate buffer").
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "emb_a2a_internal.h"
+
+namespace emba2a {
+namespace {
+
+// ------------------------------------------------------------------------------------ PTX
+__device__ __forceinline__ float4 ld_row4(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_out4(float* p, const float4& v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& x) {
+  a.x = __fadd_rn(a.x, x.x);
+  a.y = __fadd_rn(a.y, x.y);
+  a.z = __fadd_rn(a.z, x.z);
+  a.w = __fadd_rn(a.w, x.w);
+}
+
+// ------------------------------------------------------------------- gather + pool (a3, a4)
+// Predicated 16-byte read-only row load: when !pred the destination is +0.0 (no memory access).
+__device__ __forceinline__ float4 ld_row4_pred(const float4* p, bool pred) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+
+__device__ __forceinline__ int lds_s32(unsigned addr) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// One bag per group of LPB lanes; lane c of the group owns float4 columns c, c+LPB, ... (NV of
+// them).  Per batch of U rows: the U row ids are read first (shared memory if staged, else
+// global), then all U x NV row loads are issued (predicated, zero-filled past the bag's end), then
+// the adds run in bag order.  acc starts at +0.0 and can never become -0.0, so adding the +0.0
+// padding leaves it unchanged: the result is the oracle's ascending-order fp32 sum bit for bit.
+template <int LPB, int NV, int U, bool SMEM_IDX>
+__device__ __forceinline__ void pool_bag(const float4* __restrict__ tab, int D4, unsigned idx_s,
+                                         const int* __restrict__ idx_g, int lo, int hi, int lane,
+                                         float4 (&acc)[NV]) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool colok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) colok[v] = (lane + v * LPB) < D4;
+  for (int k = lo; k < hi; k += U) {
+    const int n = hi - k;
+    int row[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = (u < n) ? k + u : k;     // always a valid id; the load is predicated off
+      row[u] = SMEM_IDX ? lds_s32(idx_s + 4u * (unsigned)kk) : __ldg(idx_g + kk);
+    }
+    float4 x[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4* r = tab + (size_t)(unsigned)row[u] * D4 + lane;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_row4_pred(r + v * LPB, colok[v] && (u < n));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) add4(acc[v], x[u][v]);
+  }
+}
+
+// ------------------------------------------------------------------------- mbarrier PTX
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  // default semantics: .release at .cta scope -- orders this thread's prior writes (incl. its
+  // global stores) before the phase completion observed by a waiter.
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+#ifndef EMBA2A_WAIT_SPIN
+#define EMBA2A_WAIT_SPIN 0
+#endif
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  // default semantics: .acquire at .cta scope
+#if EMBA2A_WAIT_SPIN
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(unsigned dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+// Arrive on `bar` once all of this thread's prior cp.async copies have landed (counts as one of
+// the barrier's expected arrivals: .noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// One pipeline stage: a run of <= C consecutive bags of one chunk whose indices fit idx_cap.
+struct StageHdr {
+  int end;            // 1: no more work (consumers exit)
+  int s, t;           // destination rank, local table
+  int row0;           // destination-local row of the stage's first bag
+  int nb;             // bags in this stage
+  int base;           // offsets value of the first bag (indices[base] is the stage's first)
+  int staged;         // indices copied to shared memory
+  int remote;         // fused, s != r: count the stage's bags toward its slice when consumed
+  int slice_id, slice_bags;
+  long long j0;       // global sample of the first bag
+  float* out_base;    // fused: recv_s[parity]; pool: send
+  unsigned long long* flag;
+};
+
+// Per-CTA timeline (tooling; the paper's WG timeline, Fig. wg_profiled).  A record is
+// (cta << 40 | event << 32 | payload, %globaltimer ns).  Events: 0 CTA start, 1 chunk ticket
+// (payload = ticket), 2 stage ready, 3 stage released (payload = 1 if it completed a remote
+// slice and signalled), 4 consumers done, 5 receive wait done.
+__device__ __forceinline__ void trace_ev(const KParams& P, unsigned event, unsigned payload) {
+  if (P.trace == nullptr) return;
+  const unsigned long long i = atomicAdd(P.trace, 1ull);
+  if ((long long)i >= P.trace_cap) return;
+  P.trace[2 + 2 * i] = ((unsigned long long)blockIdx.x << 40) |
+                       ((unsigned long long)event << 32) | payload;
+  P.trace[3 + 2 * i] = globaltimer();
+}
+
+__device__ __forceinline__ int warp_bcast(int v, int src = 0) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+__device__ __forceinline__ unsigned long long atom_add_acqrel_gpu(unsigned long long* p,
+                                                                  unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v)
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------- fused / pool
+// FUSED=true: rows a1..a8.  FUSED=false: the baseline's local-staging pool kernel.
+//
+// Persistent, warp-specialised CTA (fixed grid <= max occupancy, a task loop over logical
+// work in comm-aware order).  Work is handed out as CHUNKS of C bags (C | S) so load balance is
+// fine-grained, while communication is signalled per SLICE of S bags:
+//   warp 0 (producer)  takes chunk tickets in order (CTA c starts with chunk c; later tickets
+//                      come from an atomic counter, prefetched one ahead) -- so chunks START in
+//                      the remote-first, staggered order of row a1 -- and stages each chunk's CSR
+//                      offsets (prefetched in registers) and contiguous index range into a ring
+//                      of NS shared-memory stages (a2).  When the consumers have released a stage
+//                      of a remote slice it makes their stores visible system-wide and adds the
+//                      stage's bags to the slice's counter; the CTA whose add completes the slice
+//                      releases the destination's arrival counter (a7) -- the paper's
+//                      last-finisher WG_Done / sliceRdy protocol across CTAs.
+//   warps 1..C         gather/pool/store the bags of each stage (a3-a6) and arrive on the
+//   (consumers)        stage's empty barrier; no CTA-wide barrier inside the loop, so a fast lane
+//                      group moves on to the next stage while slow ones finish ("make forward
+//                      progress after setting WG_Done instead of waiting on an inter-WG barrier",
+//                      P:151).
+template <int LPB, int NV, int U, bool FUSED, int MINB>
+__global__ void __launch_bounds__(288, MINB) emb_a2a_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned long long full_bar[kMaxStages], empty_bar[kMaxStages];
+  __shared__ int last_cta;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane32 = tid & 31;
+  const int NS = P.nstages;
+  const int nconsumer = blockDim.x - 32;
+  const size_t stage_bytes = (size_t)P.stage_bytes;
+  auto hdr = [&](int st) { return reinterpret_cast<StageHdr*>(smem_raw + st * stage_bytes); };
+  auto soff = [&](int st) {
+    return reinterpret_cast<int*>(smem_raw + st * stage_bytes + sizeof(StageHdr));
+  };
+  auto sidx = [&](int st) { return soff(st) + P.C + 1; };
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full_bar[i], 64);   // 32 producer arrivals + 32 cp.async completions
+      mbar_init(&empty_bar[i], (unsigned)nconsumer);
+    }
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ===================================================================== producer
+    if (lane32 == 0) trace_ev(P, 0, 0);
+    int u = 0;   // stage uses so far
+    // wait until consumers released use v; for a remote slice, publish its bags (a7)
+    auto recycle = [&](int v) {
+      const int st = v % NS;
+      mbar_wait(&empty_bar[st], (unsigned)((v / NS) & 1));
+      unsigned signalled = 0;
+      if (FUSED && lane32 == 0) {
+        const StageHdr* h = hdr(st);
+        if (h->remote) {
+          // every consumer store of this stage happens-before this point (mbarrier
+          // release/acquire); make them visible system-wide before counting them (R#25)
+          fence_acq_rel_sys();
+          const unsigned long long old =
+              atom_add_acqrel_gpu(P.slice_cnt + h->slice_id, (unsigned long long)h->nb);
+          if (old + (unsigned long long)h->nb ==
+              P.epoch * (unsigned long long)h->slice_bags && h->s != P.skip_to) {
+            if (P.delay_ns > 0) {
+              const unsigned long long t0 = globaltimer();
+              while (globaltimer() - t0 < (unsigned long long)P.delay_ns) __nanosleep(1000);
+            }
+            red_release_sys_add(h->flag, 1ull);   // P:151 PUT -> fence -> sliceRdy
+            signalled = 1;
+          }
+        }
+      }
+      if (lane32 == 0) trace_ev(P, 3, signalled);
+      __syncwarp();
+    };
+    // chunks: CTA c takes c, c + gridDim.x, c + 2*gridDim.x, ...  All CTAs walk the chunk list
+    // in lock-step, so chunks start in the remote-first, staggered order of row a1; the static
+    // stride needs no ticket atomics on the latency-critical path.  The next chunk's offsets are
+    // prefetched into registers (lane q holds off[q] and off[32 + q]).
+    int ticket = (int)blockIdx.x;
+    int k, s, t, i0, nb;
+    int o0 = 0, o1 = 0;
+    auto load_offsets = [&](int tk, int& kk, int& ss, int& tt, int& ii, int& nn, int& a,
+                            int& b2) {
+      decode_unit(P, tk, P.C, P.chunk_base, kk, ss, tt, ii, nn);
+      const int* offg = P.offsets + (long long)tt * P.B + P.part[ss] + ii;
+      if (lane32 <= nn) a = __ldg(offg + lane32);
+      if (32 + lane32 <= nn) b2 = __ldg(offg + 32 + lane32);
+    };
+    if (ticket < P.nchunks) load_offsets(ticket, k, s, t, i0, nb, o0, o1);
+    while (ticket < P.nchunks) {
+      const int tk_next = ticket + (int)gridDim.x;
+      int k2 = 0, s2 = 0, t2 = 0, i02 = 0, nb2 = 0, p0 = 0, p1 = 0;
+      if (tk_next < P.nchunks) load_offsets(tk_next, k2, s2, t2, i02, nb2, p0, p1);
+      if (lane32 == 0) trace_ev(P, 1, (unsigned)ticket);
+      int slice_id = 0, slice_bags = 0;
+      if (FUSED) slice_of_chunk(P, k, s, t, i0, slice_id, slice_bags);
+      const long long j0 = P.part[s] + i0;
+      for (int cb = 0; cb < nb;) {    // usually one stage per chunk
+        const int st = u % NS;
+        if (u >= NS) recycle(u - NS);
+        int* so = soff(st);
+        int n = nb - cb;
+        // offsets cb..cb+n of the chunk, from registers (lane q <-> off[q], off[32+q])
+        const int base = warp_bcast(cb < 32 ? o0 : o1, cb & 31);
+        int cnt = warp_bcast(nb < 32 ? o0 : o1, nb & 31) - base;
+        int staged = 1;
+        if (cnt > P.idx_cap) {   // shrink the run to what fits; a lone huge bag reads global
+          int m = 0;
+          for (int q = 1; q <= n; ++q) {
+            const int e = cb + q;
+            const int v = warp_bcast(e < 32 ? o0 : o1, e & 31);
+            if (v - base <= P.idx_cap) m = q;
+          }
+          if (m == 0) { m = 1; staged = 0; }
+          n = m;
+          const int e = cb + n;
+          cnt = warp_bcast(e < 32 ? o0 : o1, e & 31) - base;
+        }
+        // stage-local offsets
+        if (lane32 >= cb && lane32 <= cb + n) so[lane32 - cb] = o0;
+        if (32 + lane32 >= cb && 32 + lane32 <= cb + n) so[32 + lane32 - cb] = o1;
+        if (staged) {   // asynchronous, coalesced copy; completion tracked by full_bar[st]
+          const int* ig = P.indices + base;
+          const unsigned si = smem_u32(sidx(st));
+          for (int q = lane32; q < cnt; q += 32) cp_async4(si + 4u * (unsigned)q, ig + q);
+        }
+        if (lane32 == 0) {
+          StageHdr* h = hdr(st);
+          h->end = 0; h->s = s; h->t = t; h->row0 = i0 + cb; h->nb = n; h->base = base;
+          h->staged = staged; h->j0 = j0 + cb;
+          h->remote = (FUSED && s != P.r) ? 1 : 0;
+          h->slice_id = slice_id;
+          h->slice_bags = slice_bags;
+          if (FUSED) {
+            h->out_base = P.peers->recv[s][P.parity];
+            h->flag = P.peers->flag_out[s];
+          } else {
+            h->out_base = P.send;
+            h->flag = nullptr;
+          }
+        }
+        __syncwarp();
+        mbar_arrive(&full_bar[st]);
+        cp_async_mbar_arrive(&full_bar[st]);
+        if (lane32 == 0) trace_ev(P, 2, (unsigned)u);
+        cb += n;
+        ++u;
+      }
+      ticket = tk_next;
+      k = k2; s = s2; t = t2; i0 = i02; nb = nb2; o0 = p0; o1 = p1;
+    }
+    // end marker, then drain: every outstanding stage is consumed and published
+    {
+      const int st = u % NS;
+      if (u >= NS) recycle(u - NS);
+      if (lane32 == 0) hdr(st)->end = 1;
+      __syncwarp();
+      mbar_arrive(&full_bar[st]);
+      cp_async_mbar_arrive(&full_bar[st]);
+      for (int v = (u - NS + 1 > 0 ? u - NS + 1 : 0); v < u; ++v) recycle(v);
+    }
+  } else {
+    // ===================================================================== consumers
+    const int ctid = tid - 32;
+    const int lane = ctid % LPB;
+    const int group = ctid / LPB;
+    const int ngroups = nconsumer / LPB;
+    const int D = P.D4 * 4;
+    for (int u = 0;; ++u) {
+      const int st = u % NS;
+      mbar_wait(&full_bar[st], (unsigned)((u / NS) & 1));
+      const StageHdr* h = hdr(st);
+      if (h->end) break;
+      const int nb = h->nb, base = h->base, t = h->t;
+      const int* so = soff(st);
+      const bool staged = h->staged;
+      const unsigned idx_s = smem_u32(sidx(st));
+      const int* idx_g = P.indices + base;
+      const float4* tab = reinterpret_cast<const float4*>(P.tables[t]);
+      for (int b = group; b < nb; b += ngroups) {
+        float4 acc[NV];
+        const int lo = so[b] - base, hi = so[b + 1] - base;
+        if (staged)
+          pool_bag<LPB, NV, U, true>(tab, P.D4, idx_s, idx_g, lo, hi, lane, acc);
+        else
+          pool_bag<LPB, NV, U, false>(tab, P.D4, idx_s, idx_g, lo, hi, lane, acc);
+        float* dst;
+        if (FUSED)   // a5: row (row0 + b) of s's [b_s][G*D], column block g = toff + t
+          dst = h->out_base + ((long long)(h->row0 + b) * P.G + (P.toff + t)) * D;
+        else         // staging [B][T][D] by global row: block of s starts at p_s*T*D
+          dst = h->out_base + ((h->j0 + b) * P.T + t) * (long long)D;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
+          const int c = lane + v * LPB;
+          if (c < P.D4) st_out4(dst + 4 * c, acc[v]);
+        }
+      }
+      mbar_arrive(&empty_bar[st]);
+    }
+    if (ctid == 0) trace_ev(P, 4, 0);
+  }
+
+  // last-finisher detection over CTAs (the WG_Done role): the atomic's return value
+  // decides (R#18).  The last CTA resets the ticket and done counters for the next launch (every
+  // CTA has already drawn its final ticket and counted itself).
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int prev = atomicAdd(P.done, 1u);
+    last_cta = (prev == (unsigned int)gridDim.x - 1u);
+    if (last_cta) {
+      *P.done = 0u;
+      *P.ticket = 0u;
+    }
+  }
+  __syncthreads();
+  if constexpr (FUSED) {
+  if (P.W == 1 || !last_cta) return;
+
+  // a8: receive-side completion wait, one thread per source rank
+  for (int src = tid; src < P.W; src += blockDim.x) {
+    if (src == P.r) continue;
+    const unsigned long long target = P.epoch * (unsigned long long)P.peers->n_in[src];
+    const unsigned long long* f = P.flags_in + (size_t)src * kFlagStride;
+    const unsigned long long t0 = globaltimer();
+    unsigned int backoff = 32;
+    while (ld_acquire_sys(f) < target) {
+      if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
+        atomicExch(P.err, 0x100 | src);   // surfaces as EMB_A2A_ETIMEOUT on the next call
+        break;
+      }
+      __nanosleep(backoff);
+      if (backoff < 1024) backoff <<= 1;
+    }
+  }
+  if (tid == 0) trace_ev(P, 5, 0);
+  }
+}
+
+// Cross-rank device barrier (bench tooling, not the hot path): every rank adds 1 to each peer's
+// barrier counter with release semantics, then waits for W-1 arrivals on its own counter.  Lets
+// all ranks' timed regions start within the fabric round trip instead of host launch jitter.
+__global__ void barrier_kernel(const DevPeers* __restrict__ peers, unsigned long long* own, int W,
+                               int r, unsigned long long target, long long timeout_ns, int* err) {
+  const int q = threadIdx.x;
+  if (q < W && q != r) red_release_sys_add(peers->barrier_out[q], 1ull);
+  if (q == 0) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(own) < target) {
+      if (globaltimer() - t0 > (unsigned long long)timeout_ns) {
+        atomicExch(err, 0x200);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+__global__ void slice_plan_kernel(const __grid_constant__ KParams P, int* out) {
+  const int ticket = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ticket >= P.nslices) return;   // slice-level decode (the signal units)
+  int s, t, i0, nb;
+  decode_slice(P, ticket, s, t, i0, nb);
+  out[4 * ticket + 0] = s;
+  out[4 * ticket + 1] = t;
+  out[4 * ticket + 2] = i0;
+  out[4 * ticket + 3] = nb;
+}
+
+// Validate mode: offsets[0] = 0, non-decreasing, offsets[TB] = nnz, 0 <= idx < rows[t].
+__global__ void validate_kernel(const int* __restrict__ indices, const int* __restrict__ offsets,
+                                long long nnz, long long TB, long long B,
+                                const long long* __restrict__ rows, int* err) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q < TB) {
+    const int lo = offsets[q], hi = offsets[q + 1];
+    if (hi < lo || lo < 0 || (long long)hi > nnz) { atomicExch(err, 1); return; }
+    const long long rmax = rows[q / B];
+    for (int k = lo; k < hi; ++k) {
+      const int v = indices[k];
+      if (v < 0 || (long long)v >= rmax) { atomicExch(err, 2); return; }
+    }
+  }
+  if (q == 0 && (offsets[0] != 0 || (long long)offsets[TB] != nnz)) atomicExch(err, 1);
+}
+
+// ------------------------------------------------------------------------- dispatch
+template <bool FUSED>
+using KFn = void (*)(const KParams);
+
+// MINB: minimum resident CTAs of 256 threads per SM the register allocation must allow
+// (2 -> <= 128 registers, 4 -> <= 64): the MLP-vs-occupancy trade-off of P:280.
+template <int LPB, int NV, int U, bool FUSED>
+KFn<FUSED> pick_minb(int minb) {
+  if (minb >= 4) return emb_a2a_kernel<LPB, NV, U, FUSED, 4>;
+  return emb_a2a_kernel<LPB, NV, U, FUSED, 2>;
+}
+
+template <int LPB, int NV, bool FUSED>
+KFn<FUSED> pick_u(int U, int minb) {
+  switch (U) {
+    case 2: return pick_minb<LPB, NV, 2, FUSED>(minb);
+    case 4: return pick_minb<LPB, NV, 4, FUSED>(minb);
+    case 16: return pick_minb<LPB, NV, 16, FUSED>(minb);
+    default: return pick_minb<LPB, NV, 8, FUSED>(minb);
+  }
+}
+
+// lanes per bag = min(32, next_pow2(D/4)); float4s per lane = ceil(D4 / LPB) rounded to 1,2,4,8
+template <bool FUSED>
+KFn<FUSED> pick(int D4, int U, int minb, int* lpb_out) {
+  int lpb = 1;
+  while (lpb < D4 && lpb < 32) lpb <<= 1;
+  *lpb_out = lpb;
+  if (lpb < 32) {
+    switch (lpb) {
+      case 1: return pick_u<1, 1, FUSED>(U, minb);
+      case 2: return pick_u<2, 1, FUSED>(U, minb);
+      case 4: return pick_u<4, 1, FUSED>(U, minb);
+      case 8: return pick_u<8, 1, FUSED>(U, minb);
+      default: return pick_u<16, 1, FUSED>(U, minb);
+    }
+  }
+  const int nv = (D4 + 31) / 32;
+  if (nv <= 1) return pick_u<32, 1, FUSED>(U, minb);
+  if (nv <= 2) return pick_u<32, 2, FUSED>(U, minb);
+  if (nv <= 4) return pick_u<32, 4, FUSED>(U, minb);
+  return pick_u<32, 8, FUSED>(U, minb);
+}
+
+int auto_unroll(int D4) {
+  const int nv = (D4 + 31) / 32;
+  if (nv <= 1) return 8;
+  if (nv <= 2) return 4;
+  return 2;
+}
+
+size_t stage_bytes(int C, int idx_cap) {
+  const size_t b = sizeof(StageHdr) + (size_t)(C + 1 + idx_cap) * sizeof(int);
+  return (b + 15) / 16 * 16;
+}
+
+template <bool FUSED>
+cudaError_t launch(KParams P, const LaunchCfg& c, cudaStream_t st, int* grid_out) {
+  cudaGetLastError();   // never report someone else's stale error as ours
+  const int U = c.unroll > 0 ? c.unroll : auto_unroll(P.D4);
+  int lpb = 0;
+  KFn<FUSED> fn = pick<FUSED>(P.D4, U, c.minb, &lpb);
+  P.stage_bytes = (int)stage_bytes(P.C, P.idx_cap);
+  const size_t smem = (size_t)P.stage_bytes * P.nstages;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+  }
+  const int threads = c.threads + 32;      // consumers + one producer warp
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  if (c.ctas_per_sm > 0 && c.ctas_per_sm < occ) occ = c.ctas_per_sm;
+  long long grid = (long long)sms * occ;
+  const long long want = P.nchunks > 0 ? P.nchunks : 1;
+  if (grid > want) grid = want;
+  if (grid_out) *grid_out = (int)grid;
+  fn<<<(unsigned)grid, threads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_fused(const KParams& P, const LaunchCfg& c, cudaStream_t st, int* grid_out) {
+  return launch<true>(P, c, st, grid_out);
+}
+
+cudaError_t launch_pool_local(const KParams& P, const LaunchCfg& c, cudaStream_t st) {
+  if (P.nchunks == 0) return cudaSuccess;
+  return launch<false>(P, c, st, nullptr);
+}
+
+cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,
+                           unsigned long long target, long long timeout_ns, int* err,
+                           cudaStream_t st) {
+  barrier_kernel<<<1, ((W + 31) / 32) * 32, 0, st>>>(peers, own_counter, W, r, target, timeout_ns,
+                                                     err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slice_plan(const KParams& P, int* out, cudaStream_t st) {
+  if (P.nslices == 0) return cudaSuccess;
+  slice_plan_kernel<<<(P.nslices + 255) / 256, 256, 0, st>>>(P, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const int* indices, const int* offsets, long long nnz, long long TB,
+                            long long B, int T, const long long* rows_dev, int* err_dev,
+                            cudaStream_t st) {
+  (void)T;
+  const long long blocks = (TB + 255) / 256;
+  validate_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(indices, offsets, nnz, TB,
+                                                                        B, rows_dev, err_dev);
+  return cudaGetLastError();
+}
+
+}  // namespace emba2a

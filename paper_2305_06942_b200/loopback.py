@@ -1,0 +1,53 @@
+"""W virtual ranks of the fused op on ONE device (single-GPU loopback, SURVEY.md Sec 4 tier T1).
+
+Each virtual rank is a full EmbA2A handle with its own symmetric region; "peer" pointers are
+same-process raw pointers, so the kernels, counters and waits are exactly the multi-GPU ones
+with NVLink replaced by local HBM.  Forwards go on W separate streams so the W fused kernels
+can be co-resident (a rank's receive wait needs its peers' kernels to make progress).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from .emb_a2a import EmbA2A, LocalGroup, run_ranks
+
+
+class LoopbackGroup:
+    def __init__(self, world_size: int, device="cuda:0", options: Optional[dict] = None):
+        self.W = world_size
+        self.device = torch.device(device)
+        self.group = LocalGroup(world_size)
+        self.handles: List[EmbA2A] = [
+            EmbA2A(r, world_size, self.device, self.group.allgather_for(r), options)
+            for r in range(world_size)]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(world_size)]
+
+    def set_option(self, key: str, value: int) -> None:
+        for h in self.handles:
+            h.set_option(key, value)
+
+    def register_tables(self, tables: Sequence[Sequence[torch.Tensor]], global_batch: int,
+                        partition: Optional[Sequence[int]] = None, dim: Optional[int] = None):
+        if dim is not None:
+            for h in self.handles:
+                h.set_dim_hint(dim)
+        run_ranks(lambda r: self.handles[r].register_tables(tables[r], global_batch, partition),
+                  self.W)
+
+    def forward(self, indices: Sequence[torch.Tensor], offsets: Sequence[torch.Tensor],
+                sync: bool = True) -> List[torch.Tensor]:
+        cur = torch.cuda.current_stream(self.device)
+        outs = []
+        for r, h in enumerate(self.handles):
+            self.streams[r].wait_stream(cur)
+            outs.append(h.forward(indices[r], offsets[r], stream=self.streams[r]))
+        for s in self.streams:
+            cur.wait_stream(s)
+        if sync:
+            torch.cuda.synchronize(self.device)
+        return outs
+
+    def destroy(self):
+        run_ranks(lambda r: self.handles[r].destroy(), self.W)
