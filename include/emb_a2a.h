@@ -123,20 +123,25 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *   "slice"        S, pooled vectors per slice, >= 1 (P:147 user parameter; default 32)
  *   "order"        0 comm-aware staggered (default), 1 comm-aware ascending, 2 oblivious
  *                  (set before register_tables)
- *   "chunk"        bags per work ticket, 1..63 (default 8; the largest divisor of S not above
+ *   "chunk"        bags per work ticket, 1..63 (default 16; the largest divisor of S not above
  *                  it is used): load-balance granularity, independent of the signal slice S
  *                  (set before register_tables)
  *   "threads"      consumer threads per CTA, multiple of 32 in [32, 256] (default 256); each
  *                  CTA also has one producer warp
- *   "minb"         register budget: 2 (<= 128 regs/thread) or 4 (<= 64 regs/thread) CTAs/SM
  *   "timeout_ms"   receive-wait timeout (default 10000)
  *   "validate"     1 = check indices/offsets on device before each forward (sync)
- *   "unroll"       rows in flight per lane group: 0 = auto, else 2, 4, 8, 16
- *   "stages"       shared-memory pipeline depth per CTA, 2..8 (default 4)
+ *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
+ *                  fewer lanes per bag keeps more bags in flight per warp
+ *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)
+ *                  1 = TMA tile::gather4 of whole rows into shared memory (measured ~2x slower
+ *                  for 256 B - 1 KB rows on B200; kept as an option)
+ *   "stage_kb"     TMA mode: KiB of table rows per pipeline stage (default 32); a bag with more
+ *                  rows than a stage holds is gathered with LDGs
+ *   "stages"       shared-memory pipeline depth per CTA, 2..8 (default 4; reduced to fit 227 KB)
  *   "ctas_per_sm"  persistent grid size per SM: 0 = max occupancy (P:280 occupancy study)
- *   "idx_cap"      indices per pipeline stage (default 2048); a slice whose bags need more is
- *                  split over several stages, and a single bag longer than this reads its
- *                  indices from global memory
+ *   "idx_cap"      LSU mode: indices per pipeline stage (default 2048); a chunk whose bags need
+ *                  more is split over several stages, and a single bag longer than this reads
+ *                  its indices from global memory
  *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
  *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
  *   "debug_delay_ns"  test knob: CTAs sleep this long before signalling (stress tests)

@@ -12,6 +12,12 @@ constexpr int kMaxW = EMB_A2A_MAX_WORLD;
 // Per-source arrival counters are padded to 128 B so concurrent writers never share a line.
 constexpr int kFlagStride = 16;  // uint64 words
 constexpr int kMaxStages = 8;    // shared-memory pipeline depth cap
+constexpr int kMaxSmemTables = 256;  // table pointers cached in shared memory per CTA
+
+// A CUtensorMap (TMA descriptor): 128 opaque bytes, 64-B aligned.
+struct alignas(64) TmaDesc {
+  unsigned char bytes[128];
+};
 
 // Where peer s's receive buffers and our counter inside peer s's region live.  Device-resident,
 // written once per registration (the roc_shmem_ptr table of).
@@ -28,6 +34,7 @@ struct KParams {
   const int* indices;
   const int* offsets;
   const float* const* tables;   // device array of T pointers
+  const TmaDesc* tmaps;         // device array of T tensor maps (TMA gather mode)
   float* send;                  // pool_local staging base ([B][T][D] by global row)
   const DevPeers* peers;
   unsigned long long* flags_in; // own counters, index src * kFlagStride
@@ -41,8 +48,12 @@ struct KParams {
   unsigned long long epoch;     // 1-based forward number
   long long timeout_ns;
   long long delay_ns;
-  int W, r, T, D4, G, toff, S, C, order, nslices, nchunks, idx_cap, nstages, stage_bytes,
-      skip_to, parity;
+  int W, r, T, D4, G, toff, S, C, order, nslices, nchunks, nstages, skip_to, parity;
+  int tma;            // 1: rows via TMA gather4 into shared memory; 0: per-lane LDG gathers
+  int ncb, box4;      // TMA: column blocks per row and float4s per block (D4 = ncb * box4)
+  int stage_bytes;    // shared memory per pipeline stage
+  int payload_off;    // offset of the rows / indices inside a stage
+  int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
   int chunk_base[kMaxW + 1];    // first chunk of destination ordinal k; [W] = nchunks
@@ -92,11 +103,13 @@ __host__ __device__ inline void slice_of_chunk(const KParams& P, int k, int s, i
   slice_bags = rem < P.S ? (int)rem : P.S;
 }
 
+// Fill stage_bytes / payload_off / payload_cap for P.tma, P.C, P.D4 (kernels.cu).
+void stage_layout(KParams& P, int stage_kb, int idx_cap);
+
 struct LaunchCfg {
   int threads;      // consumer threads per CTA (+1 producer warp)
-  int unroll;       // 0 auto
+  int vec;          // float4s per lane (0 auto)
   int ctas_per_sm;  // persistent grid: 0 = max occupancy
-  int minb;         // register budget: 2 (<=128 regs) or 4 (<=64 regs) CTAs of 256 per SM
 };
 
 // Launchers (kernels.cu).  Return cudaError_t of the launch.

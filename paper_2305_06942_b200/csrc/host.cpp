@@ -3,6 +3,8 @@
 // Owns: the symmetric receive region ("symmetric heap"; here a library-owned cudaMalloc
 // exported with cudaIpcGetMemHandle), the peer pointer table (roc_shmem_ptr analogue),
 // epochs, validation and error state.  Every step of the forward runs in kernels.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
 
@@ -80,8 +82,9 @@ struct emb_a2a {
 
   // options
   int64_t S = 32, order = 0, threads = 256, timeout_ms = 10000, validate = 0, unroll = 0;
-  int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, minb = 2;
-  int64_t chunk = 8;
+  int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, tma = 0;
+  int64_t stage_kb = 32, vec = 0;
+  int64_t chunk = 16;
   int64_t trace_cap = 0;                 // records; 0 = tracing off
   unsigned long long* d_trace = nullptr;
 
@@ -94,6 +97,8 @@ struct emb_a2a {
   DevPeers host_peers{};
   DevPeers* d_peers = nullptr;
   const float** d_tables = nullptr;
+  TmaDesc* d_tmaps = nullptr;            // one TMA descriptor per local table
+  int ncb = 1, box4 = 1;
   long long* d_rows = nullptr;
   unsigned int* d_done = nullptr;        // [fused done, fused ticket, pool done, pool ticket]
   unsigned long long* d_slice_cnt = nullptr;   // per-slice completed-bag counters
@@ -160,6 +165,8 @@ void release_registration(emb_a2a* h) {
   if (h->region) cudaFree(h->region);
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->d_tables) cudaFree(h->d_tables);
+  if (h->d_tmaps) cudaFree(h->d_tmaps);
+  h->d_tmaps = nullptr;
   if (h->d_rows) cudaFree(h->d_rows);
   if (h->d_done) cudaFree(h->d_done);
   if (h->d_slice_cnt) cudaFree(h->d_slice_cnt);
@@ -225,6 +232,10 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) 
   P.indices = indices;
   P.offsets = offsets;
   P.tables = h->d_tables;
+  P.tmaps = h->d_tmaps;
+  P.tma = (int)h->tma;
+  P.ncb = h->ncb;
+  P.box4 = h->box4;
   P.peers = h->d_peers;
   P.flags_in = h->flags;
   P.done = h->d_done;
@@ -245,19 +256,54 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) 
   P.S = (int)h->S;
   P.order = (int)h->order;
   P.nslices = h->nslices;
-  P.idx_cap = (int)h->idx_cap;
   P.C = h->C;
   P.nchunks = h->nchunks;
   P.slice_cnt = h->d_slice_cnt;
   P.nstages = (int)h->stages;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
+  stage_layout(P, (int)h->stage_kb, (int)h->idx_cap);
   for (int s = 0; s <= h->W; ++s) {
     P.part[s] = h->part[s];
     P.slice_base[s] = h->slice_base[s];
     P.chunk_base[s] = h->chunk_base[s];
   }
   return P;
+}
+
+// TMA descriptors for the local tables: 2-D [rows][D] fp32, box {box, 1} so that one
+// tile::gather4 moves 4 arbitrary rows x box columns.  box = D / ncb <= 256 elements.
+int make_tensor_maps(emb_a2a* h, const float* const* tables) {
+  h->ncb = 1;
+  while (h->D / h->ncb > 256 || h->D % h->ncb != 0 || (h->D / h->ncb) % 4 != 0) ++h->ncb;
+  h->box4 = h->D / h->ncb / 4;
+  if (h->T == 0) return EMB_A2A_OK;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return fail(h, EMB_A2A_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  std::vector<TmaDesc> maps(h->T);
+  for (int t = 0; t < h->T; ++t) {
+    cuuint64_t gdim[2] = {(cuuint64_t)h->D, (cuuint64_t)h->rows[t]};
+    cuuint64_t gstride[1] = {(cuuint64_t)h->D * 4};
+    cuuint32_t box[2] = {(cuuint32_t)(h->box4 * 4), 1};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(&maps[t]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        2, const_cast<float*>(tables[t]), gdim, gstride, box, estride,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(h, EMB_A2A_EINVAL, "cuTensorMapEncodeTiled(table %d) failed (%d)", t, (int)r);
+  }
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_tmaps, sizeof(TmaDesc) * h->T));
+  CUDA_TRY(h, cudaMemcpy(h->d_tmaps, maps.data(), sizeof(TmaDesc) * h->T,
+                         cudaMemcpyHostToDevice));
+  return EMB_A2A_OK;
 }
 
 int push_peers(emb_a2a* h) {
@@ -502,6 +548,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
                            cudaMemcpyHostToDevice));
   }
   compute_slices(h);
+  {
+    const int rc_maps = make_tensor_maps(h, tables);
+    if (rc_maps) return rc_maps;
+  }
   CUDA_TRY(h, cudaMalloc((void**)&h->d_slice_cnt, sizeof(unsigned long long) *
                                                       std::max(1, h->nslices)));
   CUDA_TRY(h, cudaMemset(h->d_slice_cnt, 0, sizeof(unsigned long long) *
@@ -535,7 +585,7 @@ int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets
   }
   h->epoch += 1;
   KParams P = make_params(h, indices, offsets);
-  LaunchCfg c{(int)h->threads, (int)h->unroll, (int)h->ctas_per_sm, (int)h->minb};
+  LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
   cudaError_t e = launch_fused(P, c, st, &h->last_grid);
   if (e != cudaSuccess) {
     h->poisoned = true;
@@ -611,7 +661,7 @@ int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offs
   P.send = send;
   P.done = h->d_done + 2;      // own counters: may run concurrently with a forward's kernel
   P.ticket = h->d_done + 3;
-  LaunchCfg c{(int)h->threads, (int)h->unroll, (int)h->ctas_per_sm, (int)h->minb};
+  LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
   cudaError_t e = launch_pool_local(P, c, st);
   if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "pool kernel launch: %s",
                                     cudaGetErrorString(e));
@@ -664,16 +714,18 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     h->timeout_ms = v;
   } else if (k == "validate") {
     h->validate = v ? 1 : 0;
-  } else if (k == "unroll") {
-    if (!(v == 0 || v == 2 || v == 4 || v == 8 || v == 16))
-      return fail(h, EMB_A2A_EINVAL, "unroll in {0,2,4,8,16}");
-    h->unroll = v;
   } else if (k == "idx_cap") {
     if (v < 0 || v > 16384) return fail(h, EMB_A2A_EINVAL, "idx_cap in [0, 16384]");
     h->idx_cap = v;
-  } else if (k == "minb") {
-    if (v != 2 && v != 4) return fail(h, EMB_A2A_EINVAL, "minb in {2, 4}");
-    h->minb = v;
+  } else if (k == "vec") {
+    if (!(v == 0 || v == 1 || v == 2 || v == 4 || v == 8))
+      return fail(h, EMB_A2A_EINVAL, "vec in {0, 1, 2, 4, 8}");
+    h->vec = v;
+  } else if (k == "tma") {
+    h->tma = v ? 1 : 0;
+  } else if (k == "stage_kb") {
+    if (v < 1 || v > 200) return fail(h, EMB_A2A_EINVAL, "stage_kb in [1, 200]");
+    h->stage_kb = v;
   } else if (k == "stages") {
     if (v < 2 || v > kMaxStages) return fail(h, EMB_A2A_EINVAL, "stages in [2, %d]", kMaxStages);
     h->stages = v;
@@ -709,12 +761,13 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "threads") *v = h->threads;
   else if (k == "timeout_ms") *v = h->timeout_ms;
   else if (k == "validate") *v = h->validate;
-  else if (k == "unroll") *v = h->unroll;
   else if (k == "idx_cap") *v = h->idx_cap;
   else if (k == "stages") *v = h->stages;
   else if (k == "chunk") *v = h->chunk;
   else if (k == "trace") *v = h->trace_cap;
-  else if (k == "minb") *v = h->minb;
+  else if (k == "tma") *v = h->tma;
+  else if (k == "vec") *v = h->vec;
+  else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
   else if (k == "debug_delay_ns") *v = h->delay_ns;
   else if (k == "debug_skip_signal_to") *v = h->skip_to;

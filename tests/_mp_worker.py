@@ -1,0 +1,78 @@
+"""Worker bodies for multi-process tests (spawned; must be importable)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def init_gloo(rank, world, port):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+def cpu_allgather_worker(rank, world, port, q):
+    """Host logic of the N>1 path on CPU: the torch.distributed bootstrap all-gather and the
+    per-rank sampled oracle check that bench/tests use (each rank checks its own rows)."""
+    import numpy as np
+    dist = init_gloo(rank, world, port)
+    from paper_2305_06942_b200.emb_a2a import torch_allgather   # noqa: E402
+    import oracle
+    import synth
+    ag = torch_allgather()
+    payload = bytes([rank]) * 7
+    out = ag(payload)
+    ok_ag = out == b"".join(bytes([r]) * 7 for r in range(world))
+    cfg = synth.config_for("tiny", W=world)
+    csr = synth.gen_all_csr(cfg, 0)
+    tabs = [synth.table_values_host(cfg.table_seed, 0, g, cfg.R, cfg.D) for g in range(cfg.G)]
+    full = oracle.emb_a2a(cfg.part, cfg.D, cfg.B, cfg.T, tabs, [c[0] for c in csr],
+                          [c[1] for c in csr])
+    b = int(cfg.part[rank + 1] - cfg.part[rank])
+    mine = oracle.emb_a2a_rows(cfg.table_seed, 0, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
+                               [c[0] for c in csr], [c[1] for c in csr], rank, np.arange(b))
+    ok_rows = bool(np.array_equal(mine, full[rank]))
+    # max-over-ranks reduction as bench.py does it
+    import torch
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok_max = float(t.item()) == float(world)
+    q.put((rank, ok_ag, ok_rows, ok_max))
+    dist.destroy_process_group()
+
+
+def gpu_ipc_worker(rank, world, port, q):
+    """Real cross-process cudaIpc path: W processes on ONE GPU, gloo bootstrap."""
+    import numpy as np
+    import torch
+    dist = init_gloo(rank, world, port)
+    import oracle
+    import synth
+    from paper_2305_06942_b200 import EmbA2A, torch_allgather
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    cfg = synth.config_for("tiny", W=world)
+    csr = synth.gen_all_csr(cfg, 0)
+    tabs_host = [synth.table_values_host(cfg.table_seed, 0, g, cfg.R, cfg.D) for g in range(cfg.G)]
+    h = EmbA2A(rank, world, dev, torch_allgather(), {"timeout_ms": 60000, "slice": 5})
+    mine = [torch.from_numpy(tabs_host[cfg.toff(rank) + t]).to(dev) for t in range(cfg.T[rank])]
+    h.register_tables(mine, cfg.B)
+    ref = oracle.emb_a2a(cfg.part, cfg.D, cfg.B, cfg.T, tabs_host, [c[0] for c in csr],
+                         [c[1] for c in csr])
+    idx = torch.from_numpy(csr[rank][0]).to(dev)
+    off = torch.from_numpy(csr[rank][1]).to(dev)
+    ok = True
+    for e in range(3):
+        out = h.forward(idx, off)
+        torch.cuda.synchronize()
+        ok &= bool(np.array_equal(out.cpu().numpy(), ref[rank]))
+    flags = h.read_flags()
+    ok_flags = all(int(flags[src]) == 3 * oracle.signal_count(src, rank, cfg.T, cfg.part, 5)
+                   for src in range(world))
+    h.destroy()
+    q.put((rank, ok, ok_flags))
+    dist.destroy_process_group()

@@ -91,8 +91,9 @@ def test_random_configs_vs_oracle(seed):
     g.destroy()
 
 
+@pytest.mark.parametrize("tma,vec", [(0, 0), (1, 0), (0, 2), (0, 4)])
 @pytest.mark.parametrize("D", [4, 8, 12, 16, 60, 64, 92, 128, 132, 256, 384, 512, 1024])
-def test_all_lane_mappings(D):
+def test_all_lane_mappings(D, tma, vec):
     """Every lane mapping (LPB 1..32, NV 1..8) incl. masked columns (D/4 not a power of 2)."""
     rng = np.random.default_rng(D)
     W, T, B = 2, [2, 3], 24
@@ -106,7 +107,7 @@ def test_all_lane_mappings(D):
         idx.append(i)
         off.append(o)
     p = Problem(W, T, D, B, synth.even_partition(B, W), tables, idx, off)
-    g = make_group(p)
+    g = make_group(p, {"tma": tma, "vec": vec})
     check(g.forward(*dev_csr(p)), oracle_out(p), exact=True)
     g.destroy()
 
@@ -115,8 +116,11 @@ def test_all_lane_mappings(D):
 
 @pytest.mark.parametrize("opts", [
     {"slice": 1}, {"slice": 7}, {"slice": 32}, {"slice": 100000},
-    {"order": 1}, {"order": 2}, {"threads": 64}, {"threads": 128}, {"minb": 4}, {"stages": 2}, {"stages": 8}, {"ctas_per_sm": 1}, {"threads": 32},
-    {"unroll": 2}, {"unroll": 4}, {"unroll": 16}, {"idx_cap": 0}, {"idx_cap": 5}, {"idx_cap": 64}, {"chunk": 1}, {"chunk": 3}, {"chunk": 63}, {"chunk": 32, "slice": 64},
+    {"order": 1}, {"order": 2}, {"threads": 64}, {"threads": 128}, {"threads": 32},
+    {"stages": 2}, {"stages": 8}, {"ctas_per_sm": 1}, {"idx_cap": 0}, {"idx_cap": 5},
+    {"idx_cap": 64}, {"threads": 64, "chunk": 5}, {"tma": 1}, {"tma": 1, "stage_kb": 1},
+    {"tma": 1, "stage_kb": 3}, {"tma": 1, "stages": 8, "stage_kb": 64}, {"chunk": 1}, {"chunk": 3}, {"chunk": 63},
+    {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32},
 ])
 def test_results_invariant_to_tunables(opts):
     """Slice size, schedule, CTA size, unroll and index staging must not change any bit."""

@@ -31,11 +31,14 @@ def main():
     ap.add_argument("--alpha", type=float, default=1.05)
     ap.add_argument("--pool", action="store_true", help="also time pool_local")
     ap.add_argument("--B", type=int, default=0, help="override the global batch")
+    ap.add_argument("--R", type=int, default=0, help="override rows per table")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--flush-mode", default="write", choices=["write", "read", "sleep"])
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     over = {"B": args.B} if args.B else {}
+    if args.R:
+        over["R"] = args.R
     cfg = synth.config_for(args.config, W=args.W, alpha=args.alpha, **over)
     assert cfg.W == 1, "sweep runs one real rank"
     batches = [synth.gen_rank_csr(cfg, 0, k) for k in range(args.batches)]
@@ -55,9 +58,14 @@ def main():
     for combo in itertools.product(*vals):
         opts = dict(zip(keys, combo))
         h = EmbA2A(0, 1, dev, LocalGroup(1).allgather_for(0))
-        for k, v in opts.items():
-            h.set_option(k, v)
-        h.register_tables(tables, cfg.B)
+        try:
+            for k, v in opts.items():
+                h.set_option(k, v)
+            h.register_tables(tables, cfg.B)
+            h.forward(d_in[0][0], d_in[0][1])
+        except Exception as e:   # invalid combination (e.g. too much shared memory)
+            print(json.dumps({"config": cfg.name, "opts": opts, "error": str(e)[:200]}), flush=True)
+            continue
         st = torch.cuda.current_stream()
 
         def run(fn):
