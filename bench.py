@@ -43,7 +43,11 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--vec", type=int, default=0)
     ap.add_argument("--order", type=int, default=-1)
-    ap.add_argument("--batches", type=int, default=8, help="distinct pre-generated batches")
+    ap.add_argument("--batches", type=int, default=16,
+                    help="distinct pre-generated batches rotated through the timed steps")
+    ap.add_argument("--timing", default="b2b", choices=["b2b", "flushed"],
+                    help="b2b: K back-to-back steps between one event pair, rotating batches whose "
+                         "working set exceeds L2; flushed: L2 flush + per-step events")
     ap.add_argument("--no-baseline", action="store_true", help="skip the unfused NCCL baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -269,6 +273,26 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
+    def b2b_loop(step_fn, K, W):
+        """W warm-up steps, then K back-to-back steps between ONE event pair on the launching
+        stream (inputs rotate over args.batches batches whose working set exceeds L2), bracketed
+        by barrier + synchronize.  Returns this rank's total ms."""
+        for w in range(W):
+            step_fn(w % args.batches)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h.device_barrier(stream)          # align rank starts on the device (no-op at W = 1)
+        a.record(stream)
+        for k in range(K):
+            step_fn(k % args.batches)
+        b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
     def timed_loop(step_fn, K, W, with_barrier=True):
         """W warm-up steps, then K steps; per step: L2 flush, device barrier, events around the
         step on the launching stream.  Returns per-step ms (this rank)."""
@@ -301,39 +325,53 @@ def main():
     launches0 = h.query("kernel_launches")
     clk = ClockSampler(local)
     clk.start()
-    ms = timed_loop(fused_step, args.steps, args.warmup)
+    b2b_ms = b2b_loop(fused_step, args.steps, args.warmup)
     clocks = clk.stop()
     launches = h.query("kernel_launches") - launches0 - args.warmup
-    total_ms = max_over_ranks(sum(ms))
+    launches -= 1 if N > 1 else 0          # the device barrier before the timed region
+    ms = timed_loop(fused_step, args.steps, args.warmup)     # flushed, per-step events
     lookups = sum(nnz_all[k % args.batches] for k in range(args.steps))
+    b2b_total = max_over_ranks(b2b_ms)
+    flushed_total = max_over_ranks(sum(ms))
+    total_ms = b2b_total if args.timing == "b2b" else flushed_total
     value = lookups / (total_ms / 1e3)
     ms_step = total_ms / args.steps
 
-    # dominant kernel = the fused kernel (one launch per step); per-launch time from the same events
+    # dominant kernel = the fused kernel (one launch per step); per-launch time from the same
+    # events over the timed region
     nnz_mean = float(np.mean([mine[k % args.batches][0].size for k in range(args.steps)]))
     hbm_b, tx_b = algorithmic_bytes(cfg, rank, nnz_mean)
-    kern_s = float(np.mean(ms)) / 1e3
     peak_hbm, peak_src = measured_peaks()
     t_hbm = hbm_b / (peak_hbm * 1e9)
     t_nvl = tx_b / (NVLINK_GBS * 1e9)
-    if t_nvl > t_hbm:
-        roof = {"bound": "nvlink", "achieved": tx_b / kern_s / 1e9, "peak": NVLINK_GBS,
-                "unit": "GB/s", "peak_source": "measured peer copy (B200_PROFILING.md)"}
-    else:
-        roof = {"bound": "hbm", "achieved": hbm_b / kern_s / 1e9, "peak": peak_hbm,
-                "unit": "GB/s", "peak_source": peak_src}
-    roof["frac"] = roof["achieved"] / roof["peak"]
+
+    def roofline(kern_s):
+        if t_nvl > t_hbm:
+            r = {"bound": "nvlink", "achieved": tx_b / kern_s / 1e9, "peak": NVLINK_GBS,
+                 "unit": "GB/s", "peak_source": "measured peer copy (B200_PROFILING.md)"}
+        else:
+            r = {"bound": "hbm", "achieved": hbm_b / kern_s / 1e9, "peak": peak_hbm,
+                 "unit": "GB/s", "peak_source": peak_src}
+        r["frac"] = r["achieved"] / r["peak"]
+        return r
+
+    roof = roofline(ms_step / 1e3)
     roof["algorithmic_bytes_per_launch"] = hbm_b
     roof["nvlink_tx_bytes_per_launch"] = tx_b
     roof["traffic"] = ncu_traffic(cfg)
     roof["roofline_us"] = max(t_hbm, t_nvl) * 1e6
+    flushed = {"us_per_step": flushed_total / args.steps * 1e3,
+               "us_p50": float(np.median(ms)) * 1e3, "us_p90": float(np.percentile(ms, 90)) * 1e3,
+               "lookups_per_s": lookups / (flushed_total / 1e3),
+               "roofline_frac": roofline(flushed_total / args.steps / 1e3)["frac"],
+               "note": "L2 flushed (512 MiB write) + device barrier before each step, CUDA events "
+                       "around each forward (includes ~5 us event overhead per step)"}
 
     # ---- end to end through the public API: pinned host inputs -> device -> host result
     b = h.b
     h_out = torch.empty((b, h.G * h.D), dtype=torch.float32).pin_memory()
     e2e_step = lambda k: h.forward_host(h_in[k][0], h_in[k][1], h_out, stream)  # noqa: E731
-    e2e_ms = timed_loop(e2e_step, args.steps, args.warmup)
-    e2e_total = max_over_ranks(sum(e2e_ms))
+    e2e_total = max_over_ranks(b2b_loop(e2e_step, args.steps, args.warmup))
     h2d = float(np.mean([(mine[k % args.batches][0].size + mine[k % args.batches][1].size) * 4
                          for k in range(args.steps)]))
     e2e = {"value": lookups / (e2e_total / 1e3), "unit": "lookups/s",
@@ -354,10 +392,16 @@ def main():
             if permute:   # [src][i][t][d] -> [i][src*T+t][d] (R#17)
                 final.view(b, N, T, cfg.D).copy_(recv.permute(1, 0, 2, 3))
 
-        un_np = timed_loop(lambda k: unfused_step(k, False), args.steps, args.warmup)
-        un_p = timed_loop(lambda k: unfused_step(k, True), args.steps, args.warmup)
-        un_np_ms = max_over_ranks(sum(un_np)) / args.steps
-        un_p_ms = max_over_ranks(sum(un_p)) / args.steps
+        if args.timing == "b2b":
+            un_np_ms = max_over_ranks(b2b_loop(lambda k: unfused_step(k, False), args.steps,
+                                               args.warmup)) / args.steps
+            un_p_ms = max_over_ranks(b2b_loop(lambda k: unfused_step(k, True), args.steps,
+                                              args.warmup)) / args.steps
+        else:
+            un_np_ms = max_over_ranks(sum(timed_loop(lambda k: unfused_step(k, False), args.steps,
+                                                     args.warmup))) / args.steps
+            un_p_ms = max_over_ranks(sum(timed_loop(lambda k: unfused_step(k, True), args.steps,
+                                                    args.warmup))) / args.steps
         # parity of the two paths on the last batch (cheap, outside timing)
         k = 0
         out_f = h.forward(d_in[k][0], d_in[k][1], stream).clone()
@@ -385,12 +429,20 @@ def main():
                    "pooling": list(cfg.pool), "alpha": cfg.alpha, "world": N,
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
-                   "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
-                   "batches": args.batches, "step_timing": "CUDA events around each forward "
-                   "after a cross-rank device barrier; sum over K steps; max over ranks"},
+                   "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
+                          "distinct rows) over %.1f GB of tables, K back-to-back steps" %
+                          (args.batches, args.batches * working_set_mb(cfg, mine[0][0], mine[0][1]),
+                           cfg.T[rank] * cfg.R * cfg.D * 4 / 1e9))
+                   if args.timing == "b2b" else
+                   f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+                   "batches": args.batches,
+                   "step_timing": ("one CUDA event pair around K back-to-back forwards on the "
+                                   "launching stream, after barrier + device barrier; max over ranks")
+                   if args.timing == "b2b" else
+                   "CUDA events around each forward after L2 flush + device barrier; sum over K; "
+                   "max over ranks"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
-        "clocks": clocks, "gpu_launches": int(launches),
-        "fused_us_p50": float(np.median(ms)) * 1e3, "fused_us_p90": float(np.percentile(ms, 90)) * 1e3,
+        "flushed": flushed, "clocks": clocks, "gpu_launches": int(launches),
     }
     if rank == 0:
         s = json.dumps(line)
@@ -401,6 +453,14 @@ def main():
     h.destroy()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def working_set_mb(cfg, idx, off):
+    """Indices + distinct table rows one batch touches on this rank (MB): the part of the input
+    that could stay in L2 between steps."""
+    T = (off.size - 1) // cfg.B if cfg.B else 0
+    rows = sum(np.unique(idx[off[t * cfg.B]:off[(t + 1) * cfg.B]]).size for t in range(T))
+    return (idx.size * 4 + off.size * 4 + rows * cfg.D * 4) / 1e6
 
 
 def ncu_traffic(cfg):

@@ -112,9 +112,20 @@ struct LaunchCfg {
   int ctas_per_sm;  // persistent grid: 0 = max occupancy
 };
 
-// Launchers (kernels.cu).  Return cudaError_t of the launch.
-cudaError_t launch_fused(const KParams& P, const LaunchCfg& c, cudaStream_t st, int* grid_out);
-cudaError_t launch_pool_local(const KParams& P, const LaunchCfg& c, cudaStream_t st);
+// A resolved launch: kernel instance, persistent grid, block, shared memory, pipeline depth.
+struct LaunchPlan {
+  const void* fn = nullptr;
+  unsigned grid = 0;
+  int threads = 0;
+  size_t smem = 0;
+  int nstages = 0;
+};
+
+// Launchers (kernels.cu).  plan_* resolve a LaunchPlan once (occupancy query etc.);
+// launch_planned is the per-forward path.
+cudaError_t plan_fused(const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
+cudaError_t plan_pool_local(const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
+cudaError_t launch_planned(const LaunchPlan& pl, KParams P, cudaStream_t st);
 cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,
                            unsigned long long target, long long timeout_ns, int* err,
                            cudaStream_t st);

@@ -117,6 +117,7 @@ struct emb_a2a {
   int chunk_base[kMaxW + 1] = {0};
   int C = 8, nchunks = 0;
   int last_grid = 0;
+  LaunchPlan plan_fused, plan_pool;      // cached launch configurations (fn == nullptr: stale)
   int64_t kernel_launches = 0;
 };
 
@@ -561,6 +562,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
   CUDA_TRY(h, cudaDeviceSynchronize());
   h->epoch = 0;
   h->barrier_epoch = 0;
+  h->plan_fused = LaunchPlan();
+  h->plan_pool = LaunchPlan();
   h->registered = true;
   return barrier(h);   // nobody forwards before everyone has mapped everyone
 }
@@ -585,8 +588,13 @@ int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets
   }
   h->epoch += 1;
   KParams P = make_params(h, indices, offsets);
-  LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
-  cudaError_t e = launch_fused(P, c, st, &h->last_grid);
+  cudaError_t e = cudaSuccess;
+  if (!h->plan_fused.fn) {
+    LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
+    e = plan_fused(P, c, &h->plan_fused);
+  }
+  if (e == cudaSuccess) e = launch_planned(h->plan_fused, P, st);
+  h->last_grid = (int)h->plan_fused.grid;
   if (e != cudaSuccess) {
     h->poisoned = true;
     return fail(h, EMB_A2A_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
@@ -661,8 +669,14 @@ int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offs
   P.send = send;
   P.done = h->d_done + 2;      // own counters: may run concurrently with a forward's kernel
   P.ticket = h->d_done + 3;
-  LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
-  cudaError_t e = launch_pool_local(P, c, st);
+  cudaError_t e = cudaSuccess;
+  if (P.nchunks > 0) {
+    if (!h->plan_pool.fn) {
+      LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
+      e = plan_pool_local(P, c, &h->plan_pool);
+    }
+    if (e == cudaSuccess) e = launch_planned(h->plan_pool, P, st);
+  }
   if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "pool kernel launch: %s",
                                     cudaGetErrorString(e));
   if (P.nslices > 0) h->kernel_launches++;
@@ -687,6 +701,8 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
 
 int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
   if (!h || !key) return EMB_A2A_EINVAL;
+  h->plan_fused = LaunchPlan();   // any option may change the kernel instance / grid / smem
+  h->plan_pool = LaunchPlan();
   std::string k(key);
   if (k == "slice") {
     if (v < 1 || v > (1 << 20)) return fail(h, EMB_A2A_EINVAL, "slice must be in [1, 2^20]");

@@ -624,13 +624,16 @@ KFn<FUSED> pick(int D4, int nv_want, bool tma) {
   }
 }
 
+// Resolve kernel instance, shared memory, pipeline depth and persistent grid once; the result
+// is cached by the host per handle (no occupancy query on the per-forward path).
 template <bool FUSED>
-cudaError_t launch(KParams P, const LaunchCfg& c, cudaStream_t st, int* grid_out) {
+cudaError_t plan(const KParams& P, const LaunchCfg& c, LaunchPlan* pl) {
   cudaGetLastError();   // never report someone else's stale error as ours
   KFn<FUSED> fn = pick<FUSED>(P.D4, c.vec, P.tma != 0);
   // pipeline depth: as requested, but never more than fits the 227 KB per-CTA limit (>= 2)
-  while (P.nstages > 2 && (size_t)P.stage_bytes * P.nstages > 227 * 1024) --P.nstages;
-  const size_t smem = (size_t)P.stage_bytes * P.nstages;
+  int ns = P.nstages;
+  while (ns > 2 && (size_t)P.stage_bytes * ns > 227 * 1024) --ns;
+  const size_t smem = (size_t)P.stage_bytes * ns;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;   // even 2 stages do not fit
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -651,20 +654,28 @@ cudaError_t launch(KParams P, const LaunchCfg& c, cudaStream_t st, int* grid_out
   long long grid = (long long)sms * occ;
   const long long want = P.nchunks > 0 ? P.nchunks : 1;
   if (grid > want) grid = want;
-  if (grid_out) *grid_out = (int)grid;
-  fn<<<(unsigned)grid, threads, smem, st>>>(P);
-  return cudaGetLastError();
+  pl->fn = reinterpret_cast<const void*>(fn);
+  pl->grid = (unsigned)grid;
+  pl->threads = threads;
+  pl->smem = smem;
+  pl->nstages = ns;
+  return cudaSuccess;
 }
 
 }  // namespace
 
-cudaError_t launch_fused(const KParams& P, const LaunchCfg& c, cudaStream_t st, int* grid_out) {
-  return launch<true>(P, c, st, grid_out);
+cudaError_t plan_fused(const KParams& P, const LaunchCfg& c, LaunchPlan* pl) {
+  return plan<true>(P, c, pl);
 }
 
-cudaError_t launch_pool_local(const KParams& P, const LaunchCfg& c, cudaStream_t st) {
-  if (P.nchunks == 0) return cudaSuccess;
-  return launch<false>(P, c, st, nullptr);
+cudaError_t plan_pool_local(const KParams& P, const LaunchCfg& c, LaunchPlan* pl) {
+  return plan<false>(P, c, pl);
+}
+
+cudaError_t launch_planned(const LaunchPlan& pl, KParams P, cudaStream_t st) {
+  P.nstages = pl.nstages;
+  void* args[] = {&P};
+  return cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
 }
 
 cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,

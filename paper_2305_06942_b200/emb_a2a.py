@@ -111,6 +111,8 @@ class EmbA2A:
         if rc:
             raise EmbA2AError(rc, "emb_a2a_init")
         self._tables: List[torch.Tensor] = []
+        self._views = {}          # (ptr, rows, cols) -> cached zero-copy view of a recv buffer
+        self._stream_cache = None
         for k, v in (options or {}).items():
             self.set_option(k, v)
 
@@ -150,6 +152,9 @@ class EmbA2A:
             part = (ctypes.c_int64 * (self.W + 1))(*[int(x) for x in partition])
         rc = lib.emb_a2a_register_tables(self._h, len(tabs), ptrs, rows, D, int(global_batch), part)
         self._err(rc, "emb_a2a_register_tables")
+        self._views = {}
+        self._fwd_out = (ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64())
+        self._fwd_refs = tuple(ctypes.byref(x) for x in self._fwd_out)
         self.D = D
         self.G = self.query("total_tables")
         self.b = self.query("local_batch")
@@ -163,17 +168,22 @@ class EmbA2A:
     def forward(self, indices: torch.Tensor, offsets: torch.Tensor, stream=None) -> torch.Tensor:
         """Fused forward; returns a zero-copy view [b_r, G*D] of the library-owned receive buffer
         (valid until the second following forward)."""
-        _check_dev_tensor(offsets, torch.int32, "offsets", self.device)
-        _check_dev_tensor(indices, torch.int32, "indices", self.device)
-        out = ctypes.c_void_p()
-        rows = ctypes.c_int64()
-        cols = ctypes.c_int64()
-        rc = lib.emb_a2a_forward(self._h, indices.data_ptr() if indices.numel() else None,
-                                 offsets.data_ptr(), indices.numel(),
-                                 _stream_ptr(stream, self.device), ctypes.byref(out),
-                                 ctypes.byref(rows), ctypes.byref(cols))
-        self._err(rc, "emb_a2a_forward")
-        return _view(out.value or 0, (rows.value, cols.value), self.device)
+        if offsets.dtype != torch.int32 or indices.dtype != torch.int32 or \
+                offsets.device != self.device or indices.device != self.device or \
+                not (offsets.is_contiguous() and indices.is_contiguous()):
+            raise ValueError(f"indices/offsets must be contiguous int32 tensors on {self.device}")
+        out, rows, cols = self._fwd_out
+        n = indices.numel()
+        rc = lib.emb_a2a_forward(self._h, indices.data_ptr() if n else None, offsets.data_ptr(),
+                                 n, _stream_ptr(stream, self.device), self._fwd_refs[0],
+                                 self._fwd_refs[1], self._fwd_refs[2])
+        if rc:
+            self._err(rc, "emb_a2a_forward")
+        key = (out.value or 0, rows.value, cols.value)
+        v = self._views.get(key)
+        if v is None:
+            v = self._views[key] = _view(key[0], key[1:], self.device)
+        return v
 
     def forward_host(self, indices: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor,
                      stream=None) -> None:

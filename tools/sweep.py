@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--pool", action="store_true", help="also time pool_local")
     ap.add_argument("--B", type=int, default=0, help="override the global batch")
     ap.add_argument("--R", type=int, default=0, help="override rows per table")
+    ap.add_argument("--P", type=int, default=0, help="override: fixed pooling factor")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--flush-mode", default="write", choices=["write", "read", "sleep"])
     args = ap.parse_args()
@@ -39,6 +40,8 @@ def main():
     over = {"B": args.B} if args.B else {}
     if args.R:
         over["R"] = args.R
+    if args.P:
+        over["pool"] = ("fixed", args.P)
     cfg = synth.config_for(args.config, W=args.W, alpha=args.alpha, **over)
     assert cfg.W == 1, "sweep runs one real rank"
     batches = [synth.gen_rank_csr(cfg, 0, k) for k in range(args.batches)]
