@@ -227,6 +227,12 @@ def main():
     N = world
     if args.gpus != world and world == 1 and args.gpus > 1:
         raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    # EMBA2A_SHARED_GPU=1: test mode for the N>1 code path on a one-GPU box -- every rank runs on
+    # cuda:0 (cross-process cudaIpc still used), gloo bootstrap, baseline exchange via host copies.
+    # Numbers from this mode are not bench values (ranks time-share one GPU).
+    shared = os.environ.get("EMBA2A_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if not dist.is_initialized():
@@ -237,7 +243,10 @@ def main():
             s.bind(("127.0.0.1", 0))
             os.environ["MASTER_PORT"] = str(s.getsockname()[1])
             s.close()
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        if shared:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cfg = synth.config_for(args.config, W=N, alpha=args.alpha)
     # ---- inputs (all resident in HBM before timing; 8 rotating batches)
@@ -252,13 +261,13 @@ def main():
     h_in = [(torch.from_numpy(i).pin_memory(), torch.from_numpy(o).pin_memory()) for i, o in mine]
     nnz_all = []   # global lookups per batch
     for k in range(args.batches):
-        t = torch.tensor([mine[k][0].size], dtype=torch.int64, device=dev)
+        t = torch.tensor([mine[k][0].size], dtype=torch.int64, device="cpu" if shared else dev)
         dist.all_reduce(t)
         nnz_all.append(int(t.item()))
     tables = sdev.rank_tables(cfg, rank, dev)
     torch.cuda.synchronize()
 
-    h = EmbA2A(rank, N, dev, torch_allgather(None, dev))
+    h = EmbA2A(rank, N, dev, torch_allgather(None, dev), {"timeout_ms": 60000} if shared else None)
     if args.slice:
         h.set_option("slice", args.slice)
     if args.threads:
@@ -316,7 +325,7 @@ def main():
         return [a.elapsed_time(b) for a, b in evs]
 
     def max_over_ranks(x):
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -388,7 +397,12 @@ def main():
 
         def unfused_step(k, permute):
             h.pool_local(d_in[k][0], d_in[k][1], send, stream)
-            dist.all_to_all_single(recv.view(-1), send.view(-1))
+            if shared:     # gloo: exchange through host memory (test mode only)
+                r_cpu = torch.empty(recv.numel(), dtype=recv.dtype)
+                dist.all_to_all_single(r_cpu, send.view(-1).cpu())
+                recv.view(-1).copy_(r_cpu)
+            else:
+                dist.all_to_all_single(recv.view(-1), send.view(-1))
             if permute:   # [src][i][t][d] -> [i][src*T+t][d] (R#17)
                 final.view(b, N, T, cfg.D).copy_(recv.permute(1, 0, 2, 3))
 
@@ -444,6 +458,8 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
         "flushed": flushed, "clocks": clocks, "gpu_launches": int(launches),
     }
+    if shared:
+        line["test_mode"] = "EMBA2A_SHARED_GPU=1: all ranks on one GPU; not a bench value"
     if rank == 0:
         s = json.dumps(line)
         print(s, flush=True)

@@ -1,0 +1,38 @@
+"""The N>1 bench path (torchrun, one process per rank) on a one-GPU box: all ranks share cuda:0
+(EMBA2A_SHARED_GPU=1), real cross-process cudaIpc, device barrier, back-to-back and flushed
+timing loops, max-over-ranks, the unfused baseline and its bitwise check."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_torchrun_shared_gpu(n):
+    env = dict(os.environ, EMBA2A_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "4", "--warmup", "3",
+           "--config", "tiny", "--batches", "2", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == n and line["value"] > 0
+    assert line["unfused"]["fused_equals_unfused_bitwise"] is True
+    assert line["gpu_launches"] == 4
