@@ -130,6 +130,9 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  CTA also has one producer warp
  *   "timeout_ms"   receive-wait timeout (default 10000)
  *   "validate"     1 = check indices/offsets on device before each forward (sync)
+ *   "pdl"          1 = programmatic dependent launch (default): the kernel's CTAs may start while
+ *                  the previous kernel on the stream drains; all reads of inputs, counters and
+ *                  buffers wait (griddepcontrol.wait) for that kernel to complete
  *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
  *                  fewer lanes per bag keeps more bags in flight per warp
  *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)

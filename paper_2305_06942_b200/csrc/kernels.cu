@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(288, TMA ? 1 : 4)
       mbar_init(&empty_bar[i], (unsigned)nconsumer);
     }
   }
+  // Programmatic dependent launch: let the next kernel on the stream start its CTAs (launch ramp,
+  // prologue) as ours retire; it waits at griddepcontrol.wait for us to finish.
+  if (P.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = tid; i < P.T && i < kMaxSmemTables; i += blockDim.x)
     s_tab[i] = reinterpret_cast<const float4*>(P.tables[i]);
   for (int i = tid; i < P.W; i += blockDim.x) {
@@ -322,6 +325,9 @@ __global__ void __launch_bounds__(288, TMA ? 1 : 4)
       s_flag[i] = nullptr;
     }
   }
+  // Everything below reads inputs / counters / buffers a predecessor on the stream may write:
+  // wait for it (a no-op without a programmatic predecessor).
+  if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   if (warp == 0) {
@@ -675,7 +681,17 @@ cudaError_t plan_pool_local(const KParams& P, const LaunchCfg& c, LaunchPlan* pl
 cudaError_t launch_planned(const LaunchPlan& pl, KParams P, cudaStream_t st) {
   P.nstages = pl.nstages;
   void* args[] = {&P};
-  return cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(pl.threads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, pl.fn, args);
 }
 
 cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,

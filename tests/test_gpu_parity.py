@@ -120,7 +120,7 @@ def test_all_lane_mappings(D, tma, vec):
     {"stages": 2}, {"stages": 8}, {"ctas_per_sm": 1}, {"idx_cap": 0}, {"idx_cap": 5},
     {"idx_cap": 64}, {"threads": 64, "chunk": 5}, {"tma": 1}, {"tma": 1, "stage_kb": 1},
     {"tma": 1, "stage_kb": 3}, {"tma": 1, "stages": 8, "stage_kb": 64}, {"chunk": 1}, {"chunk": 3}, {"chunk": 63},
-    {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32},
+    {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32}, {"pdl": 0},
 ])
 def test_results_invariant_to_tunables(opts):
     """Slice size, schedule, CTA size, unroll and index staging must not change any bit."""
@@ -368,3 +368,20 @@ def test_full_size_sampled_rows(name, W):
     grp.destroy()
     del tabs
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("W", [1, 4])
+def test_back_to_back_forwards_without_sync(W):
+    """Two forwards on different batches issued back to back (no host sync; with programmatic
+    dependent launch the second kernel's CTAs may start while the first drains): both outputs
+    (the two double-buffer halves) must match the oracle."""
+    cfg = synth.config_for("tiny", W=W, B=64)
+    p0, p1 = from_config(cfg, 0), from_config(cfg, 1)
+    g = make_group(p0, {"slice": 4, "chunk": 2})
+    for _ in range(3):
+        a = g.forward(*dev_csr(p0), sync=False)
+        b = g.forward(*dev_csr(p1), sync=False)
+        torch.cuda.synchronize()
+        check(a, oracle_out(p0), exact=True)
+        check(b, oracle_out(p1), exact=True)
+    g.destroy()
