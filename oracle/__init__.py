@@ -63,6 +63,15 @@ def lib() -> ctypes.CDLL:
         L.oracle_emb_a2a_rows.restype = I32
         L.oracle_emb_a2a_rows.argtypes = [ctypes.c_uint64, I32, I32, P, I32, I64, P, P, P, P, P,
                                           I32, P, I64, I32, P, I32]
+        L.oracle_emb_a2a_ex.restype = I32
+        L.oracle_emb_a2a_ex.argtypes = [I32, P, I32, I64, P, P, I32, P, P, P, P, P, I32, I32, P]
+        L.oracle_emb_a2a_rows_ex.restype = I32
+        L.oracle_emb_a2a_rows_ex.argtypes = [ctypes.c_uint64, I32, I32, P, I32, I64, P, P, P, P, P,
+                                             P, I32, I32, P, I64, I32, P, I32]
+        L.oracle_bf16_to_float.restype = ctypes.c_float
+        L.oracle_bf16_to_float.argtypes = [ctypes.c_uint16]
+        L.oracle_f16_to_float.restype = ctypes.c_float
+        L.oracle_f16_to_float.argtypes = [ctypes.c_uint16]
         L.oracle_slice_plan.restype = I32
         L.oracle_slice_plan.argtypes = [I32, I32, P, I32, I64, I32, P, I64, P]
         L.oracle_signal_count.restype = I64
@@ -109,25 +118,54 @@ def _common(part, T, indices, offsets):
     return p, Ta, idx, off, nnz
 
 
+F32, BF16, F16 = 0, 1, 2
+SUM, MEAN = 0, 1
+
+
+def bf16_to_float(bits: int) -> float:
+    return float(lib().oracle_bf16_to_float(bits))
+
+
+def f16_to_float(bits: int) -> float:
+    return float(lib().oracle_f16_to_float(bits))
+
+
+def _weights(weights, idx):
+    if weights is None:
+        return None, None
+    w = [np.ascontiguousarray(a, dtype=np.float32) for a in weights]
+    w = [a if a.size else np.zeros(1, dtype=np.float32) for a in w]
+    arr = _ptr_array(w)
+    return w, arr
+
+
 def emb_a2a(part: Sequence[int], D: int, B: int, T: Sequence[int], tables: Sequence[np.ndarray],
             indices: Sequence[np.ndarray], offsets: Sequence[np.ndarray],
-            precision: int = 32) -> List[np.ndarray]:
-    """The plain definition over materialised tables (G arrays [rows_g, D] float32).
+            precision: int = 32, dtype: int = F32, weights: Optional[Sequence[np.ndarray]] = None,
+            pooling: int = SUM) -> List[np.ndarray]:
+    """The plain definition over materialised tables (G arrays [rows_g, D]).
 
+    dtype F32: float32 tables; BF16 / F16: uint16 arrays holding bfloat16 / binary16 bits.
+    weights: optional per-rank per-sample weights aligned with indices (sum pooling only).
+    pooling: SUM or MEAN (P:119 ..._sum_mean).
     Returns out_s for every destination rank s: [b_s, G*D], float32 (precision=32) or float64.
     """
     W = len(T)
     p, Ta, idx, off, nnz = _common(part, T, indices, offsets)
-    tabs = [np.ascontiguousarray(t, dtype=np.float32) for t in tables]
+    edt = np.float32 if dtype == F32 else np.uint16
+    tabs = [np.ascontiguousarray(t, dtype=edt) for t in tables]
     rows = np.array([t.shape[0] for t in tabs], dtype=np.int64)
     G = int(Ta.sum())
     assert len(tabs) == G
     dt = np.float64 if precision == 64 else np.float32
     outs = [np.full((int(p[s + 1] - p[s]), G * D), np.nan, dtype=dt) for s in range(W)]
     outs_keep = [o if o.size else np.zeros(1, dtype=dt) for o in outs]
+    wk, warr = _weights(weights, idx)
     keep = [_ptr_array(tabs), _ptr_array(idx), _ptr_array(off), _ptr_array(outs_keep)]
-    rc = lib().oracle_emb_a2a(W, _ptr(p), D, B, _ptr(Ta), _ptr(keep[0]), _ptr(rows),
-                              _ptr(keep[1]), _ptr(keep[2]), _ptr(nnz), precision, _ptr(keep[3]))
+    rc = lib().oracle_emb_a2a_ex(W, _ptr(p), D, B, _ptr(Ta), _ptr(keep[0]), dtype, _ptr(rows),
+                                 _ptr(keep[1]), _ptr(keep[2]),
+                                 _ptr(warr) if warr is not None else None, _ptr(nnz), pooling,
+                                 precision, _ptr(keep[3]))
     if rc:
         raise OracleError(rc, "emb_a2a")
     return outs
@@ -135,7 +173,8 @@ def emb_a2a(part: Sequence[int], D: int, B: int, T: Sequence[int], tables: Seque
 
 def emb_a2a_rows(seed: int, mode: int, part: Sequence[int], D: int, B: int, T: Sequence[int],
                  R: int, indices: Sequence[np.ndarray], offsets: Sequence[np.ndarray], s: int,
-                 rows_i: Sequence[int], precision: int = 32, check_inputs: bool = True) -> np.ndarray:
+                 rows_i: Sequence[int], precision: int = 32, check_inputs: bool = True,
+                 weights: Optional[Sequence[np.ndarray]] = None, pooling: int = SUM) -> np.ndarray:
     """Selected rows of out_s with procedural tables (every table has R rows)."""
     W = len(T)
     p, Ta, idx, off, nnz = _common(part, T, indices, offsets)
@@ -145,9 +184,12 @@ def emb_a2a_rows(seed: int, mode: int, part: Sequence[int], D: int, B: int, T: S
     dt = np.float64 if precision == 64 else np.float32
     out = np.full((max(sel.size, 1), G * D), np.nan, dtype=dt)
     keep = [_ptr_array(idx), _ptr_array(off), sel if sel.size else np.zeros(1, np.int64)]
-    rc = lib().oracle_emb_a2a_rows(seed, mode, W, _ptr(p), D, B, _ptr(Ta), _ptr(rows),
-                                   _ptr(keep[0]), _ptr(keep[1]), _ptr(nnz), s, _ptr(keep[2]),
-                                   sel.size, precision, _ptr(out), int(check_inputs))
+    wk, warr = _weights(weights, idx)
+    rc = lib().oracle_emb_a2a_rows_ex(seed, mode, W, _ptr(p), D, B, _ptr(Ta), _ptr(rows),
+                                      _ptr(keep[0]), _ptr(keep[1]),
+                                      _ptr(warr) if warr is not None else None, _ptr(nnz),
+                                      pooling, s, _ptr(keep[2]), sel.size, precision, _ptr(out),
+                                      int(check_inputs))
     if rc:
         raise OracleError(rc, "emb_a2a_rows")
     return out[: sel.size]

@@ -57,13 +57,18 @@ uint64_t oracle_splitmix64(uint64_t x) {
     return z ^ (z >> 31);
 }
 
-/* value of W_g[row][d]; mode 0 = fp32 grid values in [-1,1), mode 1 = exact-int in [-8,7] */
+/* value of W_g[row][d]; mode 0 = fp32 grid values in [-1,1), mode 1 = exact-int in [-8,7],
+ * mode 2 = k * 2^-7, k in [-128, 127] (exactly representable in bf16 and fp16) */
 float oracle_table_value(uint64_t seed, int mode, int64_t g, int64_t row, int64_t d) {
     uint64_t key = (((uint64_t)g * 8388608ULL + (uint64_t)row) * 1024ULL) + (uint64_t)d;
     uint64_t x = oracle_splitmix64(key ^ oracle_splitmix64(seed));
     if (mode == 1) {
         int64_t v = (int64_t)(x >> 60) - 8;
         return (float)v;
+    }
+    if (mode == 2) {
+        int64_t k = (int64_t)(x >> 56) - 128;
+        return (float)((double)k / 128.0);
     }
     int64_t q = (int64_t)(x >> 40) - 8388608;   /* [-2^23, 2^23) */
     return (float)((double)q / 8388608.0);      /* exact: |q| < 2^24 */
@@ -72,17 +77,59 @@ float oracle_table_value(uint64_t seed, int mode, int64_t g, int64_t row, int64_
 /* ------------------------------------------------------------------------------------------
  * Tables: either materialised (host arrays, row-major [rows][D]) or procedural.
  * ---------------------------------------------------------------------------------------- */
+#define ORACLE_F32 0
+#define ORACLE_BF16 1
+#define ORACLE_F16 2
+#define ORACLE_SUM 0
+#define ORACLE_MEAN 1
+
 typedef struct {
     int procedural;
     uint64_t seed;
     int mode;
-    const float* const* ptr;   /* G pointers when materialised */
+    const void* const* ptr;    /* G pointers when materialised */
+    int dtype;                 /* element type of materialised tables */
     int D;
 } tables_t;
 
+/* bfloat16 bits -> float: the bf16 value is the top 16 bits of the binary32 (exact) */
+float oracle_bf16_to_float(uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+/* IEEE binary16 bits -> float (exact; subnormals, infinities and NaN included) */
+float oracle_f16_to_float(uint16_t h) {
+    uint32_t sign = (uint32_t)(h >> 15) << 31;
+    uint32_t exp = (h >> 10) & 0x1F;
+    uint32_t man = h & 0x3FF;
+    uint32_t u;
+    if (exp == 0) {
+        if (man == 0) {
+            u = sign;
+        } else {                         /* subnormal: man * 2^-24 */
+            float f = (float)man * (1.0f / 16777216.0f);
+            memcpy(&u, &f, 4);
+            u |= sign;
+        }
+    } else if (exp == 31) {
+        u = sign | 0x7F800000u | (man << 13);
+    } else {
+        u = sign | ((exp - 15 + 127) << 23) | (man << 13);
+    }
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
 static float table_at(const tables_t* tb, int64_t g, int64_t row, int64_t d) {
     if (tb->procedural) return oracle_table_value(tb->seed, tb->mode, g, row, d);
-    return tb->ptr[g][row * tb->D + d];
+    int64_t e = row * tb->D + d;
+    if (tb->dtype == ORACLE_BF16) return oracle_bf16_to_float(((const uint16_t*)tb->ptr[g])[e]);
+    if (tb->dtype == ORACLE_F16) return oracle_f16_to_float(((const uint16_t*)tb->ptr[g])[e]);
+    return ((const float*)tb->ptr[g])[e];
 }
 
 /* ------------------------------------------------------------------------------------------
@@ -134,29 +181,40 @@ static int validate(int W, const int64_t* part, int64_t B, const int32_t* T,
 }
 
 /* ------------------------------------------------------------------------------------------
- * Sum pooling of one bag, P:119 (Sec 3.1): the embedding operator "accesses one or more vectors
- * from the embedding table and pools (reduction-like operation) them".  Ascending k, start from
- * +0.0 (R#5), one binary32 add per element (fp32: R#14).  An empty bag gives +0.0 (R#4).
+ * Pooling of one bag, P:119 (Sec 3.1): the embedding operator "accesses one or more vectors
+ * from the embedding table and pools (reduction-like operation) them" (the paper names
+ * EmbeddingBag_updateOutputKernel_sum_mean).  Ascending k, start from +0.0 (R#5), one binary32
+ * add per element (fp32: R#14); an empty bag gives +0.0 (R#4).  Optional per-sample weight w_k:
+ * acc = acc + fl(w_k * x) (R#26).  Mean: acc / L with IEEE binary32 division; empty bag 0 (R#27).
+ * bf16 / fp16 tables are converted exactly to binary32 before the add (R#28).
  * ---------------------------------------------------------------------------------------- */
-static void pool_bag_f32(const tables_t* tb, int64_t g, const int32_t* idx, int64_t lo,
-                         int64_t hi, int D, float* out) {
+static void pool_bag_f32(const tables_t* tb, int64_t g, const int32_t* idx, const float* w,
+                         int64_t lo, int64_t hi, int D, int pooling, float* out) {
     for (int d = 0; d < D; ++d) {
         float acc = +0.0f;
         for (int64_t k = lo; k < hi; ++k) {
             volatile float x = table_at(tb, g, idx[k], d);   /* volatile: no reassociation */
-            acc = acc + x;
+            if (w) {                      /* per-sample weight: product rounded, then added (R#26) */
+                volatile float y = w[k] * x;
+                acc = acc + y;
+            } else {
+                acc = acc + x;
+            }
         }
+        if (pooling == ORACLE_MEAN && hi > lo) acc = acc / (float)(hi - lo);   /* R#27 */
         out[d] = acc;
     }
 }
 
 /* The same sum in binary64: the exact-arithmetic reference used to pin the fp32 result within
  * the textbook bound |fl(sum) - sum| <= gamma_{L-1} * sum|x| (tests). */
-static void pool_bag_f64(const tables_t* tb, int64_t g, const int32_t* idx, int64_t lo,
-                         int64_t hi, int D, double* out) {
+static void pool_bag_f64(const tables_t* tb, int64_t g, const int32_t* idx, const float* w,
+                         int64_t lo, int64_t hi, int D, int pooling, double* out) {
     for (int d = 0; d < D; ++d) {
         double acc = 0.0;
-        for (int64_t k = lo; k < hi; ++k) acc = acc + (double)table_at(tb, g, idx[k], d);
+        for (int64_t k = lo; k < hi; ++k)
+            acc = acc + (w ? (double)w[k] : 1.0) * (double)table_at(tb, g, idx[k], d);
+        if (pooling == ORACLE_MEAN && hi > lo) acc = acc / (double)(hi - lo);
         out[d] = acc;
     }
 }
@@ -167,63 +225,87 @@ static void pool_bag_f64(const tables_t* tb, int64_t g, const int32_t* idx, int6
  * ---------------------------------------------------------------------------------------- */
 static void one_row(int W, const int64_t* part, int D, int64_t B, const int32_t* T,
                     const tables_t* tb, const int32_t* const* indices,
-                    const int32_t* const* offsets, int s, int64_t i, int precision,
-                    void* row_out /* G*D elements */) {
+                    const int32_t* const* offsets, const float* const* weights, int pooling,
+                    int s, int64_t i, int precision, void* row_out /* G*D elements */) {
     int64_t j = part[s] + i;
     int64_t g = 0;
     for (int r = 0; r < W; ++r) {                              /* owner rank of table g */
         for (int t = 0; t < T[r]; ++t, ++g) {                  /* g = toff_r + t (R#2) */
             int64_t lo = offsets[r][(int64_t)t * B + j];
             int64_t hi = offsets[r][(int64_t)t * B + j + 1];
+            const float* w = weights ? weights[r] : NULL;
             if (precision == 64)
-                pool_bag_f64(tb, g, indices[r], lo, hi, D, (double*)row_out + g * D);
+                pool_bag_f64(tb, g, indices[r], w, lo, hi, D, pooling, (double*)row_out + g * D);
             else
-                pool_bag_f32(tb, g, indices[r], lo, hi, D, (float*)row_out + g * D);
+                pool_bag_f32(tb, g, indices[r], w, lo, hi, D, pooling, (float*)row_out + g * D);
         }
     }
 }
 
 /* Full oracle over materialised tables.  out[s] -> [b_s][G*D], float (precision 32) or double
- * (precision 64).  Every cell is written exactly once (placement is a bijection). */
-int oracle_emb_a2a(int W, const int64_t* part, int D, int64_t B, const int32_t* T,
-                   const float* const* tables, const int64_t* rows,
-                   const int32_t* const* indices, const int32_t* const* offsets,
-                   const int64_t* nnz, int precision, void* const* out) {
+ * (precision 64).  Every cell is written exactly once (placement is a bijection).
+ * tables: G pointers to [rows_g][D] elements of `dtype` (ORACLE_F32 / BF16 / F16);
+ * weights: NULL, or W per-rank arrays of per-sample weights aligned with indices (sum only);
+ * pooling: ORACLE_SUM or ORACLE_MEAN (P:119 EmbeddingBag_..._sum_mean). */
+int oracle_emb_a2a_ex(int W, const int64_t* part, int D, int64_t B, const int32_t* T,
+                      const void* const* tables, int dtype, const int64_t* rows,
+                      const int32_t* const* indices, const int32_t* const* offsets,
+                      const float* const* weights, const int64_t* nnz, int pooling,
+                      int precision, void* const* out) {
     int rc = validate(W, part, B, T, rows, indices, offsets, nnz);
     if (rc) return rc;
+    if (weights && pooling != ORACLE_SUM) return ORACLE_EINVAL;   /* as torch: sum only */
     int64_t G = 0;
     for (int r = 0; r < W; ++r) G += T[r];
-    tables_t tb = {0, 0, 0, tables, D};
+    tables_t tb = {0, 0, 0, tables, dtype, D};
     size_t esz = precision == 64 ? sizeof(double) : sizeof(float);
     for (int s = 0; s < W; ++s)
         for (int64_t i = 0; i < part[s + 1] - part[s]; ++i)
-            one_row(W, part, D, B, T, &tb, indices, offsets, s, i, precision,
+            one_row(W, part, D, B, T, &tb, indices, offsets, weights, pooling, s, i, precision,
                     (char*)out[s] + (size_t)(i * G * D) * esz);
     return ORACLE_OK;
 }
 
+int oracle_emb_a2a(int W, const int64_t* part, int D, int64_t B, const int32_t* T,
+                   const float* const* tables, const int64_t* rows,
+                   const int32_t* const* indices, const int32_t* const* offsets,
+                   const int64_t* nnz, int precision, void* const* out) {
+    return oracle_emb_a2a_ex(W, part, D, B, T, (const void* const*)tables, ORACLE_F32, rows,
+                             indices, offsets, NULL, nnz, ORACLE_SUM, precision, out);
+}
+
 /* Selected rows of out_s with procedural tables (for full-size sampled parity).
  * sel_i: n_sel local row ids of destination s; out: [n_sel][G*D]. */
-int oracle_emb_a2a_rows(uint64_t seed, int mode, int W, const int64_t* part, int D, int64_t B,
-                        const int32_t* T, const int64_t* rows, const int32_t* const* indices,
-                        const int32_t* const* offsets, const int64_t* nnz, int s,
-                        const int64_t* sel_i, int64_t n_sel, int precision, void* out,
-                        int check_inputs) {
+int oracle_emb_a2a_rows_ex(uint64_t seed, int mode, int W, const int64_t* part, int D, int64_t B,
+                           const int32_t* T, const int64_t* rows, const int32_t* const* indices,
+                           const int32_t* const* offsets, const float* const* weights,
+                           const int64_t* nnz, int pooling, int s, const int64_t* sel_i,
+                           int64_t n_sel, int precision, void* out, int check_inputs) {
     if (check_inputs) {
         int rc = validate(W, part, B, T, rows, indices, offsets, nnz);
         if (rc) return rc;
     }
     if (s < 0 || s >= W) return ORACLE_EINVAL;
+    if (weights && pooling != ORACLE_SUM) return ORACLE_EINVAL;
     int64_t G = 0;
     for (int r = 0; r < W; ++r) G += T[r];
-    tables_t tb = {1, seed, mode, NULL, D};
+    tables_t tb = {1, seed, mode, NULL, ORACLE_F32, D};
     size_t esz = precision == 64 ? sizeof(double) : sizeof(float);
     for (int64_t q = 0; q < n_sel; ++q) {
         if (sel_i[q] < 0 || sel_i[q] >= part[s + 1] - part[s]) return ORACLE_EINVAL;
-        one_row(W, part, D, B, T, &tb, indices, offsets, s, sel_i[q], precision,
+        one_row(W, part, D, B, T, &tb, indices, offsets, weights, pooling, s, sel_i[q], precision,
                 (char*)out + (size_t)(q * G * D) * esz);
     }
     return ORACLE_OK;
+}
+
+int oracle_emb_a2a_rows(uint64_t seed, int mode, int W, const int64_t* part, int D, int64_t B,
+                        const int32_t* T, const int64_t* rows, const int32_t* const* indices,
+                        const int32_t* const* offsets, const int64_t* nnz, int s,
+                        const int64_t* sel_i, int64_t n_sel, int precision, void* out,
+                        int check_inputs) {
+    return oracle_emb_a2a_rows_ex(seed, mode, W, part, D, B, T, rows, indices, offsets, NULL, nnz,
+                                  ORACLE_SUM, s, sel_i, n_sel, precision, out, check_inputs);
 }
 
 /* ------------------------------------------------------------------------------------------

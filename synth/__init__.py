@@ -19,4 +19,7 @@ from .dlrm_gen import (  # noqa: F401
     table_values_host,
     splitmix64_np,
     zipf_cdf,
+    to_bf16_bits,
+    to_f16_bits,
+    gen_weights,
 )

@@ -224,5 +224,33 @@ def table_values_host(seed: int, mode: int, g: int, R: int, D: int) -> np.ndarra
     x = splitmix64_np(key ^ np.uint64(_splitmix64_int(seed)))
     if mode == 1:
         return ((x >> np.uint64(60)).astype(np.int64) - 8).astype(np.float32)
+    if mode == 2:    # k * 2^-7, k in [-128, 127]: exact in bfloat16 and binary16
+        return (((x >> np.uint64(56)).astype(np.int64) - 128).astype(np.float64) / 128.0).astype(np.float32)
     q = (x >> np.uint64(40)).astype(np.int64) - (1 << 23)
     return (q.astype(np.float64) * (2.0 ** -23)).astype(np.float32)
+
+
+def to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """float32 values that are exactly representable in bfloat16 -> uint16 bits (raises if not)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    if np.any(u & np.uint32(0xFFFF)):
+        raise ValueError("values are not exactly representable in bfloat16")
+    return (u >> np.uint32(16)).astype(np.uint16)
+
+
+def to_f16_bits(a: np.ndarray) -> np.ndarray:
+    """float32 values exactly representable in binary16 -> uint16 bits (raises if not)."""
+    h = np.ascontiguousarray(a, dtype=np.float32).astype(np.float16)
+    if not np.array_equal(h.astype(np.float32), a):
+        raise ValueError("values are not exactly representable in binary16")
+    return h.view(np.uint16)
+
+
+def gen_weights(cfg: ProblemConfig, r: int, nnz: int, batch: int = 0, mode: int = 0) -> np.ndarray:
+    """Per-sample weights for rank r's indices: mode 0 fp32 (x >> 40) * 2^-24 in [0, 1);
+    mode 1 small integers in [-4, 3] (products and sums stay exact)."""
+    bg = np.random.PCG64(_splitmix64_int(_substream_seed(cfg, batch, 1 << 30) ^ r))
+    x = _raw(bg, nnz)
+    if mode == 1:
+        return ((x >> np.uint64(61)).astype(np.int64) - 4).astype(np.float32)
+    return ((x >> np.uint64(40)).astype(np.float64) * 2.0 ** -24).astype(np.float32)

@@ -25,6 +25,7 @@ __global__ void fill_kernel(float* __restrict__ dst, long long n, int D, long lo
     const unsigned long long x = sm64(key ^ seed_mix);
     float v;
     if (mode == 1) v = (float)((long long)(x >> 60) - 8);
+    else if (mode == 2) v = (float)((double)((long long)(x >> 56) - 128) * (1.0 / 128.0));
     else v = (float)((double)((long long)(x >> 40) - 8388608ll) * (1.0 / 8388608.0));
     dst[e] = v;
   }
