@@ -51,6 +51,13 @@ typedef enum {
     EMB_A2A_EINDEX = 8     /* validate mode: index out of range / malformed CSR */
 } emb_a2a_status;
 
+/* Table element types.  Every element is converted exactly to fp32 before it is accumulated;
+ * the output is always fp32 (R#28). */
+typedef enum { EMB_A2A_F32 = 0, EMB_A2A_BF16 = 1, EMB_A2A_F16 = 2 } emb_a2a_dtype;
+/* Pooling (EmbeddingBag_updateOutputKernel_sum_mean): sum, or sum / bag length with IEEE
+ * fp32 division (an empty bag gives +0.0) (R#27). */
+typedef enum { EMB_A2A_SUM = 0, EMB_A2A_MEAN = 1 } emb_a2a_pooling;
+
 typedef struct emb_a2a emb_a2a_t;
 
 /* Caller-supplied all-gather over its process group (the bootstrap channel; S:86 problem
@@ -83,6 +90,13 @@ int emb_a2a_register_tables(emb_a2a_t* h, int num_local_tables, const float* con
                             const int64_t* rows, int dim, int64_t global_batch,
                             const int64_t* batch_partition);
 
+/* register_tables with a table element type (emb_a2a_dtype; tables[t] then points to
+ * [rows][dim] elements of that type, dim * element size a multiple of 16 bytes) and a pooling
+ * mode (emb_a2a_pooling).  Both must be identical on all ranks (EINVAL otherwise). */
+int emb_a2a_register_tables_ex(emb_a2a_t* h, int num_local_tables, const void* const* tables,
+                               const int64_t* rows, int dim, int table_dtype, int pooling,
+                               int64_t global_batch, const int64_t* batch_partition);
+
 /* One fused forward (collective), asynchronous on `stream` (cudaStream_t; NULL = legacy default).
  *  indices   DEVICE int32[num_indices]: the T_r tables' bags concatenated table-major; values
  *            are local row ids (0 <= idx < rows[t]).  Borrowed until the stream passes the op.
@@ -99,6 +113,13 @@ int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets
                     int64_t num_indices, void* stream, float** out, int64_t* out_rows,
                     int64_t* out_cols);
 
+/* forward with per-sample weights: weights = DEVICE float32[num_indices] aligned with indices
+ * (NULL = unweighted); pooled value = sum_k fl(w_k * x_k) in bag order (R#26).  Sum pooling only
+ * (EINVAL with mean, as torch.nn.functional.embedding_bag). */
+int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                             const float* weights, int64_t num_indices, void* stream,
+                             float** out, int64_t* out_rows, int64_t* out_cols);
+
 /* The same forward fed from HOST memory (the end-to-end path): copies h_indices / h_offsets
  * (host, ideally pinned) into library-owned device staging, runs the fused forward, and copies
  * the [b_r][G*D] float32 result into h_out (host, b_r*G*D floats), all enqueued on `stream`.
@@ -112,6 +133,11 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
  * all_to_all_single (P:250 baseline: embedding kernels + RCCL All-to-All). */
 int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
                        int64_t num_indices, void* stream, float* send);
+
+/* pool_local with per-sample weights (device float32[num_indices], NULL = unweighted). */
+int emb_a2a_pool_local_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                                const float* weights, int64_t num_indices, void* stream,
+                                float* send);
 
 /* Cross-rank device barrier on `stream` (collective; benchmark tooling, not part of the op):
  * returns immediately on the host; the stream proceeds once every rank's barrier kernel has
@@ -137,7 +163,8 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  fewer lanes per bag keeps more bags in flight per warp
  *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)
  *                  1 = TMA tile::gather4 of whole rows into shared memory (measured ~2x slower
- *                  for 256 B - 1 KB rows on B200; kept as an option)
+ *                  for 256 B - 1 KB rows on B200; kept as an option); applies to
+ *                  fp32 unweighted forwards only, others use the LDG path
  *   "stage_kb"     TMA mode: KiB of table rows per pipeline stage (default 32); a bag with more
  *                  rows than a stage holds is gathered with LDGs
  *   "stages"       shared-memory pipeline depth per CTA, 2..8 (default 4; reduced to fit 227 KB)
@@ -154,7 +181,8 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* value);
 
 /* Read-only facts about the current registration:
  *   "rank", "world_size", "device", "epoch" (forwards issued), "local_batch" (b_r),
- *   "total_tables" (G), "table_offset" (toff_r), "dim", "global_batch", "num_slices",
+ *   "total_tables" (G), "table_offset" (toff_r), "dim", "table_dtype", "pooling" (0 sum,
+ *   1 mean), "global_batch", "num_slices",
  *   "num_chunks", "chunk_bags" (C),
  *   "expected_in:<src>" (signals rank src sends here per forward), "region_bytes",
  *   "last_grid" (CTAs of the last fused launch), "kernel_launches" (total kernels launched). */

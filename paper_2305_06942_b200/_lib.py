@@ -12,6 +12,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EMBA2A_LIB") or os.path.join(_HERE, "libemba2a.so")
 
 OK, EINVAL, ESTATE, ECUDA, ENOMEM, EPEER, EBOOT, ETIMEOUT, EINDEX = range(9)
+F32, BF16, F16 = 0, 1, 2          # emb_a2a_dtype
+SUM, MEAN = 0, 1                  # emb_a2a_pooling
 MAX_WORLD = 64
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
@@ -35,9 +37,12 @@ _SIGS = {
     "emb_a2a_last_error": (ctypes.c_char_p, [_P]),
     "emb_a2a_init": (_I, [_I, _I, _I, ALLGATHER_FN, _P, ctypes.POINTER(_P)]),
     "emb_a2a_register_tables": (_I, [_P, _I, _P, _P, _I, _I64, _P]),
+    "emb_a2a_register_tables_ex": (_I, [_P, _I, _P, _P, _I, _I, _I, _I64, _P]),
     "emb_a2a_forward": (_I, [_P, _P, _P, _I64, _P, ctypes.POINTER(_P), _PI64, _PI64]),
+    "emb_a2a_forward_weighted": (_I, [_P, _P, _P, _P, _I64, _P, ctypes.POINTER(_P), _PI64, _PI64]),
     "emb_a2a_forward_host": (_I, [_P, _P, _P, _I64, _P, _P]),
     "emb_a2a_pool_local": (_I, [_P, _P, _P, _I64, _P, _P]),
+    "emb_a2a_pool_local_weighted": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
     "emb_a2a_device_barrier": (_I, [_P, _P]),
     "emb_a2a_set_option": (_I, [_P, ctypes.c_char_p, _I64]),
     "emb_a2a_get_option": (_I, [_P, ctypes.c_char_p, _PI64]),

@@ -33,7 +33,8 @@ struct DevPeers {
 struct KParams {
   const int* indices;
   const int* offsets;
-  const float* const* tables;   // device array of T pointers
+  const float* weights;         // per-sample weights aligned with indices, or NULL
+  const void* const* tables;    // device array of T pointers (element type: elem)
   const TmaDesc* tmaps;         // device array of T tensor maps (TMA gather mode)
   float* send;                  // pool_local staging base ([B][T][D] by global row)
   const DevPeers* peers;
@@ -48,9 +49,12 @@ struct KParams {
   unsigned long long epoch;     // 1-based forward number
   long long timeout_ns;
   long long delay_ns;
-  int W, r, T, D4, G, toff, S, C, order, nslices, nchunks, nstages, skip_to, parity;
+  int W, r, T, D, G, toff, S, C, order, nslices, nchunks, nstages, skip_to, parity;
+  int DU;             // 16-byte units per table row (D * element size / 16)
+  int elem;           // table element type: 0 fp32, 1 bf16, 2 fp16
+  int mean;           // 1: mean pooling (P:119 sum_mean), 0: sum
   int tma;            // 1: rows via TMA gather4 into shared memory; 0: per-lane LDG gathers
-  int ncb, box4;      // TMA: column blocks per row and float4s per block (D4 = ncb * box4)
+  int ncb, box4;      // TMA: column blocks per row and float4s per block (DU = ncb * box4)
   int stage_bytes;    // shared memory per pipeline stage
   int payload_off;    // offset of the rows / indices inside a stage
   int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
@@ -125,6 +129,14 @@ struct LaunchPlan {
 // Launchers (kernels.cu).  plan_* resolve a LaunchPlan once (occupancy query etc.);
 // launch_planned is the per-forward path.
 cudaError_t plan_fused(const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
+// per-instance-set planners (inst_*.cu) and the shared resolver (kernels.cu)
+cudaError_t plan_with(const void* fn, const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
+cudaError_t plan_f32(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
+cudaError_t plan_f32w(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
+cudaError_t plan_bf16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,
+                      LaunchPlan* pl);
+cudaError_t plan_f16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,
+                     LaunchPlan* pl);
 cudaError_t plan_pool_local(const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
 cudaError_t launch_planned(const LaunchPlan& pl, KParams P, cudaStream_t st);
 cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counter, int W, int r,

@@ -28,7 +28,7 @@ struct Meta {           // phase-1 all-gather record (problem statement, S:86-91
   int32_t rank, world, T, D;
   int64_t B;
   int64_t part[kMaxW + 1];
-  int32_t S, pad;
+  int32_t S, dtype, pooling, pad;
 };
 
 struct Handles {        // phase-2 all-gather record (symmetric region)
@@ -96,7 +96,9 @@ struct emb_a2a {
   std::vector<void*> opened;             // IPC-opened peer bases
   DevPeers host_peers{};
   DevPeers* d_peers = nullptr;
-  const float** d_tables = nullptr;
+  const void** d_tables = nullptr;
+  int elem = 0;                          // table element type (emb_a2a_dtype)
+  int mean = 0;                          // pooling (emb_a2a_pooling)
   TmaDesc* d_tmaps = nullptr;            // one TMA descriptor per local table
   int ncb = 1, box4 = 1;
   long long* d_rows = nullptr;
@@ -117,7 +119,8 @@ struct emb_a2a {
   int chunk_base[kMaxW + 1] = {0};
   int C = 8, nchunks = 0;
   int last_grid = 0;
-  LaunchPlan plan_fused, plan_pool;      // cached launch configurations (fn == nullptr: stale)
+  LaunchPlan plan_fused[2], plan_pool[2]; // cached launch configurations [weighted]
+                                          // (fn == nullptr: stale)
   int64_t kernel_launches = 0;
 };
 
@@ -227,14 +230,18 @@ void compute_slices(emb_a2a* h) {
   }
 }
 
-KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) {
+KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
+                    const float* weights) {
   KParams P;
   memset(&P, 0, sizeof(P));
   P.indices = indices;
   P.offsets = offsets;
+  P.weights = weights;
+  P.elem = h->elem;
+  P.mean = h->mean;
   P.tables = h->d_tables;
   P.tmaps = h->d_tmaps;
-  P.tma = (int)h->tma;
+  P.tma = (h->tma && h->elem == 0 && !weights) ? 1 : 0;   // TMA gather: fp32, unweighted
   P.ncb = h->ncb;
   P.box4 = h->box4;
   P.peers = h->d_peers;
@@ -251,7 +258,8 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) 
   P.W = h->W;
   P.r = h->rank;
   P.T = h->T;
-  P.D4 = h->D / 4;
+  P.D = h->D;
+  P.DU = h->D * (h->elem == 0 ? 4 : 2) / 16;
   P.G = h->G;
   P.toff = h->toff;
   P.S = (int)h->S;
@@ -275,8 +283,9 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets) 
 
 // TMA descriptors for the local tables: 2-D [rows][D] fp32, box {box, 1} so that one
 // tile::gather4 moves 4 arbitrary rows x box columns.  box = D / ncb <= 256 elements.
-int make_tensor_maps(emb_a2a* h, const float* const* tables) {
+int make_tensor_maps(emb_a2a* h, const void* const* tables) {
   h->ncb = 1;
+  if (h->elem != 0) return EMB_A2A_OK;   // TMA gather mode is fp32-only
   while (h->D / h->ncb > 256 || h->D % h->ncb != 0 || (h->D / h->ncb) % 4 != 0) ++h->ncb;
   h->box4 = h->D / h->ncb / 4;
   if (h->T == 0) return EMB_A2A_OK;
@@ -296,7 +305,7 @@ int make_tensor_maps(emb_a2a* h, const float* const* tables) {
     cuuint32_t box[2] = {(cuuint32_t)(h->box4 * 4), 1};
     cuuint32_t estride[2] = {1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap*>(&maps[t]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                        2, const_cast<float*>(tables[t]), gdim, gstride, box, estride,
+                        2, const_cast<void*>(tables[t]), gdim, gstride, box, estride,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
@@ -383,16 +392,23 @@ int emb_a2a_init(int rank, int world_size, int cuda_device, emb_a2a_allgather_fn
   return EMB_A2A_OK;
 }
 
-static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const* tables,
-                         const int64_t* rows, int dim, int64_t global_batch,
-                         const int64_t* batch_partition);
+static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* tables,
+                         const int64_t* rows, int dim, int table_dtype, int pooling,
+                         int64_t global_batch, const int64_t* batch_partition);
 
 int emb_a2a_register_tables(emb_a2a_t* h, int num_local_tables, const float* const* tables,
                             const int64_t* rows, int dim, int64_t global_batch,
                             const int64_t* batch_partition) {
+  return emb_a2a_register_tables_ex(h, num_local_tables, (const void* const*)tables, rows, dim,
+                                    EMB_A2A_F32, EMB_A2A_SUM, global_batch, batch_partition);
+}
+
+int emb_a2a_register_tables_ex(emb_a2a_t* h, int num_local_tables, const void* const* tables,
+                               const int64_t* rows, int dim, int table_dtype, int pooling,
+                               int64_t global_batch, const int64_t* batch_partition) {
   if (!h) return EMB_A2A_EINVAL;
-  const int rc = register_impl(h, num_local_tables, tables, rows, dim, global_batch,
-                               batch_partition);
+  const int rc = register_impl(h, num_local_tables, tables, rows, dim, table_dtype, pooling,
+                               global_batch, batch_partition);
   if (rc != EMB_A2A_OK && !h->registered) {
     DeviceGuard guard(h->dev);
     release_registration(h);
@@ -400,9 +416,9 @@ int emb_a2a_register_tables(emb_a2a_t* h, int num_local_tables, const float* con
   return rc;
 }
 
-static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const* tables,
-                         const int64_t* rows, int dim, int64_t global_batch,
-                         const int64_t* batch_partition) {
+static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* tables,
+                         const int64_t* rows, int dim, int table_dtype, int pooling,
+                         int64_t global_batch, const int64_t* batch_partition) {
   if (h->poisoned) return check_async(h);
   DeviceGuard guard(h->dev);
   if (h->registered) {   // collective re-registration: quiesce, barrier, tear down
@@ -415,7 +431,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
   //      mismatches are caught after the all-gather so every rank returns EINVAL together)
   int bad = 0;
   if (num_local_tables < 0 || (num_local_tables > 0 && (!tables || !rows))) bad = 1;
-  if (dim < 4 || dim > 1024 || dim % 4 != 0) bad = 1;
+  if (table_dtype < EMB_A2A_F32 || table_dtype > EMB_A2A_F16) bad = 1;
+  if (pooling != EMB_A2A_SUM && pooling != EMB_A2A_MEAN) bad = 1;
+  const int esize = table_dtype == EMB_A2A_F32 ? 4 : 2;
+  if (dim < 4 || dim > 1024 || (dim * esize) % 16 != 0) bad = 1;   // whole 16-byte units (R#9)
   if (global_batch < 0) bad = 1;
   for (int t = 0; !bad && t < num_local_tables; ++t) {
     if (rows[t] < 1 || rows[t] >= (1ll << 31)) bad = 1;
@@ -431,6 +450,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
   me.D = dim;
   me.B = global_batch;
   me.S = (int32_t)h->S;
+  me.dtype = table_dtype;
+  me.pooling = pooling;
   if (batch_partition) {
     for (int s = 0; s <= h->W; ++s) me.part[s] = batch_partition[s];
   } else if (h->W > 0 && global_batch % h->W == 0) {
@@ -451,7 +472,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
     const Meta& m = all[q];
     if (m.magic != kMagic || m.abi != EMB_A2A_ABI_VERSION || m.rank != q || m.world != h->W)
       return fail(h, EMB_A2A_EINVAL, "rank %d sent invalid registration arguments", q);
-    if (m.D != dim || m.B != global_batch || m.S != (int32_t)h->S ||
+    if (m.D != dim || m.B != global_batch || m.S != (int32_t)h->S || m.dtype != table_dtype ||
+        m.pooling != pooling ||
         memcmp(m.part, me.part, sizeof(int64_t) * (h->W + 1)) != 0)
       return fail(h, EMB_A2A_EINVAL,
                   "ranks disagree on dim / global batch / partition / slice (rank %d)", q);
@@ -464,6 +486,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
 
   h->T = num_local_tables;
   h->D = dim;
+  h->elem = table_dtype;
+  h->mean = pooling == EMB_A2A_MEAN ? 1 : 0;
   h->B = global_batch;
   h->G = (int)G;
   h->part.assign(me.part, me.part + h->W + 1);
@@ -539,12 +563,12 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
 
   // ---- device-side tables, plan, counters
   CUDA_TRY(h, cudaMalloc((void**)&h->d_peers, sizeof(DevPeers)));
-  CUDA_TRY(h, cudaMalloc((void**)&h->d_tables, sizeof(float*) * std::max(1, h->T)));
+  CUDA_TRY(h, cudaMalloc((void**)&h->d_tables, sizeof(void*) * std::max(1, h->T)));
   CUDA_TRY(h, cudaMalloc((void**)&h->d_rows, sizeof(long long) * std::max(1, h->T)));
   CUDA_TRY(h, cudaMalloc((void**)&h->d_done, 4 * sizeof(unsigned int)));
   CUDA_TRY(h, cudaMemset(h->d_done, 0, 4 * sizeof(unsigned int)));
   if (h->T > 0) {
-    CUDA_TRY(h, cudaMemcpy(h->d_tables, tables, sizeof(float*) * h->T, cudaMemcpyHostToDevice));
+    CUDA_TRY(h, cudaMemcpy(h->d_tables, tables, sizeof(void*) * h->T, cudaMemcpyHostToDevice));
     std::vector<long long> r64(rows, rows + h->T);
     CUDA_TRY(h, cudaMemcpy(h->d_rows, r64.data(), sizeof(long long) * h->T,
                            cudaMemcpyHostToDevice));
@@ -563,8 +587,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
   CUDA_TRY(h, cudaDeviceSynchronize());
   h->epoch = 0;
   h->barrier_epoch = 0;
-  h->plan_fused = LaunchPlan();
-  h->plan_pool = LaunchPlan();
+  for (int w = 0; w < 2; ++w) {
+    h->plan_fused[w] = LaunchPlan();
+    h->plan_pool[w] = LaunchPlan();
+  }
   h->registered = true;
   return barrier(h);   // nobody forwards before everyone has mapped everyone
 }
@@ -572,6 +598,13 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const float* const*
 int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
                     int64_t num_indices, void* stream, float** out, int64_t* out_rows,
                     int64_t* out_cols) {
+  return emb_a2a_forward_weighted(h, indices, offsets, nullptr, num_indices, stream, out,
+                                  out_rows, out_cols);
+}
+
+int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                             const float* weights, int64_t num_indices, void* stream,
+                             float** out, int64_t* out_rows, int64_t* out_cols) {
   if (!h) return EMB_A2A_EINVAL;
   int rc = check_async(h);
   if (rc) return rc;
@@ -587,15 +620,21 @@ int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets
     rc = run_validate(h, indices, offsets, num_indices, st);
     if (rc) return rc;
   }
+  if (weights && h->mean)
+    return fail(h, EMB_A2A_EINVAL, "per-sample weights need sum pooling (R#26)");
+  if (weights && num_indices > 0 && ((uintptr_t)weights % 4))
+    return fail(h, EMB_A2A_EINVAL, "weights must be 4-byte aligned");
   h->epoch += 1;
-  KParams P = make_params(h, indices, offsets);
+  const float* w = num_indices > 0 ? weights : nullptr;
+  KParams P = make_params(h, indices, offsets, w);
+  LaunchPlan& pl = h->plan_fused[w ? 1 : 0];
   cudaError_t e = cudaSuccess;
-  if (!h->plan_fused.fn) {
+  if (!pl.fn) {
     LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
-    e = plan_fused(P, c, &h->plan_fused);
+    e = plan_fused(P, c, &pl);
   }
-  if (e == cudaSuccess) e = launch_planned(h->plan_fused, P, st);
-  h->last_grid = (int)h->plan_fused.grid;
+  if (e == cudaSuccess) e = launch_planned(pl, P, st);
+  h->last_grid = (int)pl.grid;
   if (e != cudaSuccess) {
     h->poisoned = true;
     return fail(h, EMB_A2A_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
@@ -652,6 +691,12 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
 
 int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
                        int64_t num_indices, void* stream, float* send) {
+  return emb_a2a_pool_local_weighted(h, indices, offsets, nullptr, num_indices, stream, send);
+}
+
+int emb_a2a_pool_local_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                                const float* weights, int64_t num_indices, void* stream,
+                                float* send) {
   if (!h) return EMB_A2A_EINVAL;
   int rc = check_async(h);
   if (rc) return rc;
@@ -666,17 +711,21 @@ int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offs
     rc = run_validate(h, indices, offsets, num_indices, st);
     if (rc) return rc;
   }
-  KParams P = make_params(h, indices, offsets);
+  if (weights && h->mean)
+    return fail(h, EMB_A2A_EINVAL, "per-sample weights need sum pooling (R#26)");
+  const float* w = num_indices > 0 ? weights : nullptr;
+  KParams P = make_params(h, indices, offsets, w);
   P.send = send;
   P.done = h->d_done + 2;      // own counters: may run concurrently with a forward's kernel
   P.ticket = h->d_done + 3;
   cudaError_t e = cudaSuccess;
   if (P.nchunks > 0) {
-    if (!h->plan_pool.fn) {
+    LaunchPlan& pl = h->plan_pool[w ? 1 : 0];
+    if (!pl.fn) {
       LaunchCfg c{(int)h->threads, (int)h->vec, (int)h->ctas_per_sm};
-      e = plan_pool_local(P, c, &h->plan_pool);
+      e = plan_pool_local(P, c, &pl);
     }
-    if (e == cudaSuccess) e = launch_planned(h->plan_pool, P, st);
+    if (e == cudaSuccess) e = launch_planned(pl, P, st);
   }
   if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "pool kernel launch: %s",
                                     cudaGetErrorString(e));
@@ -702,8 +751,10 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
 
 int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
   if (!h || !key) return EMB_A2A_EINVAL;
-  h->plan_fused = LaunchPlan();   // any option may change the kernel instance / grid / smem
-  h->plan_pool = LaunchPlan();
+  for (int w = 0; w < 2; ++w) {   // any option may change the kernel instance / grid / smem
+    h->plan_fused[w] = LaunchPlan();
+    h->plan_pool[w] = LaunchPlan();
+  }
   std::string k(key);
   if (k == "slice") {
     if (v < 1 || v > (1 << 20)) return fail(h, EMB_A2A_EINVAL, "slice must be in [1, 2^20]");
@@ -809,6 +860,8 @@ int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "local_tables") *v = h->T;
   else if (k == "table_offset") *v = h->toff;
   else if (k == "dim") *v = h->D;
+  else if (k == "table_dtype") *v = h->elem;
+  else if (k == "pooling") *v = h->mean;
   else if (k == "global_batch") *v = h->B;
   else if (k == "num_slices") *v = h->nslices;
   else if (k == "num_chunks") *v = h->nchunks;
@@ -836,7 +889,7 @@ int emb_a2a_slice_plan(emb_a2a_t* h, int32_t* out, int64_t capacity, int64_t* n)
   DeviceGuard guard(h->dev);
   int* d = nullptr;
   CUDA_TRY(h, cudaMalloc((void**)&d, sizeof(int) * 4 * h->nslices));
-  KParams P = make_params(h, nullptr, nullptr);
+  KParams P = make_params(h, nullptr, nullptr, nullptr);
   cudaError_t e = launch_slice_plan(P, d, 0);
   if (e == cudaSuccess) e = cudaMemcpy(out, d, sizeof(int) * 4 * h->nslices,
                                        cudaMemcpyDeviceToHost);

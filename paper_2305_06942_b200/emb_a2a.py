@@ -135,22 +135,32 @@ class EmbA2A:
             raise EmbA2AError(rc, what, detail)
 
     # -------------------------------------------------------------- collective API
+    _DTYPES = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16, torch.float16: _lib.F16}
+
     def register_tables(self, tables: Sequence[torch.Tensor], global_batch: int,
-                        partition: Optional[Sequence[int]] = None) -> None:
-        """tables: this rank's T_r float32 [rows, D] device tensors (kept alive by the handle)."""
+                        partition: Optional[Sequence[int]] = None, pooling: str = "sum",
+                        dtype: Optional[torch.dtype] = None) -> None:
+        """tables: this rank's T_r [rows, D] device tensors, float32 / bfloat16 / float16 (kept
+        alive by the handle).  pooling: "sum" or "mean".  dtype: only needed when this
+        rank registers no tables (must match the other ranks)."""
         tabs = list(tables)
         D = int(tabs[0].shape[1]) if tabs else int(self._dim_hint)
+        tdt = tabs[0].dtype if tabs else (dtype or torch.float32)
+        if tdt not in self._DTYPES:
+            raise ValueError(f"unsupported table dtype {tdt}")
         for t in tabs:
-            _check_dev_tensor(t, torch.float32, "table", self.device)
+            _check_dev_tensor(t, tdt, "table", self.device)
             if t.dim() != 2 or t.shape[1] != D:
-                raise ValueError("tables must be [rows, D] with one D")
+                raise ValueError("tables must be [rows, D] with one D and one dtype")
         self._tables = tabs
         ptrs = (ctypes.c_void_p * max(1, len(tabs)))(*[t.data_ptr() for t in tabs])
         rows = (ctypes.c_int64 * max(1, len(tabs)))(*[t.shape[0] for t in tabs])
         part = None
         if partition is not None:
             part = (ctypes.c_int64 * (self.W + 1))(*[int(x) for x in partition])
-        rc = lib.emb_a2a_register_tables(self._h, len(tabs), ptrs, rows, D, int(global_batch), part)
+        pool = {"sum": _lib.SUM, "mean": _lib.MEAN}[pooling]
+        rc = lib.emb_a2a_register_tables_ex(self._h, len(tabs), ptrs, rows, D, self._DTYPES[tdt],
+                                            pool, int(global_batch), part)
         self._err(rc, "emb_a2a_register_tables")
         self._views = {}
         self._fwd_out = (ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64())
@@ -165,18 +175,29 @@ class EmbA2A:
         """D for a rank that registers zero tables (dim must agree across ranks)."""
         self._dim_hint = int(D)
 
-    def forward(self, indices: torch.Tensor, offsets: torch.Tensor, stream=None) -> torch.Tensor:
+    def forward(self, indices: torch.Tensor, offsets: torch.Tensor, stream=None,
+                per_sample_weights: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Fused forward; returns a zero-copy view [b_r, G*D] of the library-owned receive buffer
-        (valid until the second following forward)."""
+        (valid until the second following forward).  per_sample_weights: optional float32 device
+        tensor aligned with indices (sum pooling only)."""
         if offsets.dtype != torch.int32 or indices.dtype != torch.int32 or \
                 offsets.device != self.device or indices.device != self.device or \
                 not (offsets.is_contiguous() and indices.is_contiguous()):
             raise ValueError(f"indices/offsets must be contiguous int32 tensors on {self.device}")
         out, rows, cols = self._fwd_out
         n = indices.numel()
-        rc = lib.emb_a2a_forward(self._h, indices.data_ptr() if n else None, offsets.data_ptr(),
-                                 n, _stream_ptr(stream, self.device), self._fwd_refs[0],
-                                 self._fwd_refs[1], self._fwd_refs[2])
+        if per_sample_weights is None:
+            rc = lib.emb_a2a_forward(self._h, indices.data_ptr() if n else None,
+                                     offsets.data_ptr(), n, _stream_ptr(stream, self.device),
+                                     self._fwd_refs[0], self._fwd_refs[1], self._fwd_refs[2])
+        else:
+            _check_dev_tensor(per_sample_weights, torch.float32, "per_sample_weights", self.device)
+            if per_sample_weights.numel() != n:
+                raise ValueError("per_sample_weights must align with indices")
+            rc = lib.emb_a2a_forward_weighted(
+                self._h, indices.data_ptr() if n else None, offsets.data_ptr(),
+                per_sample_weights.data_ptr() if n else None, n, _stream_ptr(stream, self.device),
+                self._fwd_refs[0], self._fwd_refs[1], self._fwd_refs[2])
         if rc:
             self._err(rc, "emb_a2a_forward")
         key = (out.value or 0, rows.value, cols.value)
@@ -213,14 +234,19 @@ class EmbA2A:
 
     # -------------------------------------------------------------- local API
     def pool_local(self, indices: torch.Tensor, offsets: torch.Tensor, send: torch.Tensor,
-                   stream=None) -> None:
+                   stream=None, per_sample_weights: Optional[torch.Tensor] = None) -> None:
         """Unfused baseline first half: send [B, T_r, D] float32 (dest-major blocks by p_s)."""
         _check_dev_tensor(send, torch.float32, "send", self.device)
         _check_dev_tensor(offsets, torch.int32, "offsets", self.device)
         _check_dev_tensor(indices, torch.int32, "indices", self.device)
-        rc = lib.emb_a2a_pool_local(self._h, indices.data_ptr() if indices.numel() else None,
-                                    offsets.data_ptr(), indices.numel(),
-                                    _stream_ptr(stream, self.device), send.data_ptr())
+        n = indices.numel()
+        w = None
+        if per_sample_weights is not None:
+            _check_dev_tensor(per_sample_weights, torch.float32, "per_sample_weights", self.device)
+            w = per_sample_weights.data_ptr() if n else None
+        rc = lib.emb_a2a_pool_local_weighted(self._h, indices.data_ptr() if n else None,
+                                             offsets.data_ptr(), w, n,
+                                             _stream_ptr(stream, self.device), send.data_ptr())
         self._err(rc, "emb_a2a_pool_local")
 
     def set_option(self, key: str, value: int) -> None:

@@ -29,20 +29,23 @@ class LoopbackGroup:
             h.set_option(key, value)
 
     def register_tables(self, tables: Sequence[Sequence[torch.Tensor]], global_batch: int,
-                        partition: Optional[Sequence[int]] = None, dim: Optional[int] = None):
+                        partition: Optional[Sequence[int]] = None, dim: Optional[int] = None,
+                        pooling: str = "sum", dtype: Optional[torch.dtype] = None):
         if dim is not None:
             for h in self.handles:
                 h.set_dim_hint(dim)
-        run_ranks(lambda r: self.handles[r].register_tables(tables[r], global_batch, partition),
-                  self.W)
+        run_ranks(lambda r: self.handles[r].register_tables(tables[r], global_batch, partition,
+                                                            pooling, dtype), self.W)
 
     def forward(self, indices: Sequence[torch.Tensor], offsets: Sequence[torch.Tensor],
-                sync: bool = True) -> List[torch.Tensor]:
+                sync: bool = True, weights: Optional[Sequence[torch.Tensor]] = None
+                ) -> List[torch.Tensor]:
         cur = torch.cuda.current_stream(self.device)
         outs = []
         for r, h in enumerate(self.handles):
             self.streams[r].wait_stream(cur)
-            outs.append(h.forward(indices[r], offsets[r], stream=self.streams[r]))
+            outs.append(h.forward(indices[r], offsets[r], stream=self.streams[r],
+                                  per_sample_weights=None if weights is None else weights[r]))
         for s in self.streams:
             cur.wait_stream(s)
         if sync:
