@@ -149,13 +149,16 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *   "slice"        S, pooled vectors per slice, >= 1 (P:147 user parameter; default 32)
  *   "order"        0 comm-aware staggered (default), 1 comm-aware ascending, 2 oblivious
  *                  (set before register_tables)
- *   "chunk"        bags per work ticket, 1..63 (default 16; the largest divisor of S not above
+ *   "chunk"        bags per work ticket, 1..63 (default 32; the largest divisor of S not above
  *                  it is used): load-balance granularity, independent of the signal slice S
  *                  (set before register_tables)
  *   "threads"      consumer threads per CTA, multiple of 32 in [32, 256] (default 256); each
  *                  CTA also has one producer warp
  *   "timeout_ms"   receive-wait timeout (default 10000)
  *   "validate"     1 = check indices/offsets on device before each forward (sync)
+ *   "flat_below"   pipeline stages whose average bag length is below this (default 12) pool with a
+ *                  row-flattened loop (rows of several short bags in flight at once); longer
+ *                  bags use the per-bag loop.  0 = always per-bag, large = always flattened
  *   "pdl"          1 = programmatic dependent launch (default): the kernel's CTAs may start while
  *                  the previous kernel on the stream drains; all reads of inputs, counters and
  *                  buffers wait (griddepcontrol.wait) for that kernel to complete

@@ -59,6 +59,7 @@ struct KParams {
   int payload_off;    // offset of the rows / indices inside a stage
   int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
   int pdl;            // programmatic dependent launch (overlap with the stream predecessor)
+  int flat_below;     // stages whose average bag length is below this use row-flattened pooling
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
   int chunk_base[kMaxW + 1];    // first chunk of destination ordinal k; [W] = nchunks

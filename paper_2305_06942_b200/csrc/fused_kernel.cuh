@@ -276,6 +276,99 @@ __device__ __forceinline__ void pool_bag_lsu(const uint4* __restrict__ tab, int 
   }
 }
 
+// Row-flattened pooling of a contiguous block of bags [b0, b1) of one stage (the LSU path):
+// the group walks the block's rows in batches of U that may cross bag boundaries, so short bags
+// (pooling factor 1..4) still keep U rows in flight per lane.  A bag's sum is finished -- mean
+// division, store to dst0 + b*stride -- the moment its last row has been added, and the
+// accumulator restarts from +0.0, so every bag is summed alone and in ascending order (bitwise
+// the oracle's result).  Empty bags store +0.0.
+template <int ELEM, int LPB, int NV, int U, bool SMEM_IDX, bool WEIGHTED>
+__device__ __forceinline__ void pool_run_lsu(const uint4* __restrict__ tab, int DU,
+                                             unsigned idx_s, const int* __restrict__ idx_g,
+                                             unsigned w_s, const float* __restrict__ w_g,
+                                             const int* so, int base, int b0, int b1, int lane,
+                                             bool mean, float* dst0, long long stride) {
+  constexpr int EPU = Elem<ELEM>::EPU;
+  float acc[NV][EPU];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < EPU; ++e) acc[v][e] = 0.f;
+  bool colok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) colok[v] = (lane + v * LPB) < DU;
+  int cb = b0;
+  int cstart = so[b0] - base;
+  int cend = so[b0 + 1] - base;
+  const int lo_all = cstart;
+  const int hi_all = so[b1] - base;
+  auto finish = [&]() {
+    if (mean && cend > cstart) {   // R#27: IEEE binary32 division by the bag length
+      const float L = (float)(cend - cstart);
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
+    }
+    float* dst = dst0 + (long long)cb * stride;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {                             // a6: zero-copy store
+      const int c = lane + v * LPB;
+      if (c < DU) {
+#pragma unroll
+        for (int e = 0; e < EPU; e += 4)
+          st_out4(dst + EPU * c + e,
+                  make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+      }
+#pragma unroll
+      for (int e = 0; e < EPU; ++e) acc[v][e] = 0.f;
+    }
+    ++cb;
+    cstart = cend;
+    if (cb < b1) cend = so[cb + 1] - base;
+  };
+  while (cb < b1 && cend == cstart) finish();       // leading empty bags
+  for (int k = lo_all; k < hi_all; k += U) {
+    const int n = hi_all - k;
+    int row[U];
+    float wt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = (u < n) ? k + u : k;     // always a valid id; the load is predicated off
+      row[u] = SMEM_IDX ? lds_s32(idx_s + 4u * (unsigned)kk) : __ldg(idx_g + kk);
+      if (WEIGHTED) {
+        const float w = SMEM_IDX ? lds_f32(w_s + 4u * (unsigned)kk) : __ldg(w_g + kk);
+        wt[u] = (u < n) ? w : 0.f;
+      }
+    }
+    uint4 x[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4* r = tab + (size_t)(unsigned)row[u] * DU + lane;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred(r + v * LPB, colok[v] && (u < n));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u < n) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          float f[EPU];
+          unit_to_f<ELEM>(x[u][v], f);
+#pragma unroll
+          for (int e = 0; e < EPU; ++e)
+            acc[v][e] = WEIGHTED ? __fadd_rn(acc[v][e], __fmul_rn(wt[u], f[e]))
+                                 : __fadd_rn(acc[v][e], f[e]);
+        }
+        if (k + u + 1 == cend) {
+          finish();
+          while (cb < b1 && cend == cstart) finish();   // empty bags after it
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------- smem-stage pool (a4)
 // gather4 writes 4 rows x box columns per column block; TMA destinations are 128-B aligned, so a
 // block occupies cbstride = round_up(4 * boxbytes, 128) bytes and a 4-row group ncb * cbstride.
@@ -320,6 +413,7 @@ struct StageHdr {
   int nb;             // bags in this stage
   int base;           // offsets value of the first bag (indices[base] is the stage's first)
   int staged;         // payload holds this stage's rows / indices
+  int flat;           // short bags: row-flattened pooling (average length < flat_below)
   int remote;         // fused, s != r: count the stage's bags toward its slice when consumed
   int slice_id, slice_bags;
   long long j0;       // global sample of the first bag
@@ -351,13 +445,21 @@ static_assert(sizeof(StageHdr) <= kHdrBytes, "stage header too large");
 //                      group moves on to the next stage while slow ones finish ("make forward
 //                      progress after setting WG_Done instead of waiting on an inter-WG barrier",
 //                      P:151).
+#ifndef EMBA2A_LSU_MINB
+#define EMBA2A_LSU_MINB 4
+#endif
+#ifndef EMBA2A_LSU_UNITS
+#define EMBA2A_LSU_UNITS 16
+#endif
 template <int ELEM, int LPB, int NV, bool FUSED, bool TMA, bool WEIGHTED>
-__global__ void __launch_bounds__(288, TMA ? 1 : 4)
+__global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB)
     emb_a2a_kernel(const __grid_constant__ KParams P) {
   static_assert(!TMA || (ELEM == 0 && !WEIGHTED), "TMA gather: fp32 unweighted tables only");
   constexpr int EPU = Elem<ELEM>::EPU;
-  // LSU rows in flight per lane group: ~16 unit loads per lane (registers), >= 2 rows
-  constexpr int U = TMA ? 8 : (16 / NV >= 2 ? 16 / NV : 2);
+  // LSU rows in flight per lane group: ~16 unit loads per lane for the per-bag loop (long bags),
+  // ~8 for the row-flattened loop (short bags; more live state per row)
+  constexpr int U = TMA ? 8 : (EMBA2A_LSU_UNITS / NV >= 2 ? EMBA2A_LSU_UNITS / NV : 2);
+  constexpr int UF = (8 / NV >= 2 ? 8 / NV : 2);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ unsigned long long full_bar[kMaxStages], empty_bar[kMaxStages];
   __shared__ int last_cta;
@@ -481,6 +583,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : 4)
           StageHdr* h = hdr(st);
           h->end = 0; h->s = s; h->t = t; h->row0 = i0 + cb; h->nb = n; h->base = base;
           h->staged = staged; h->j0 = j0 + cb;
+          h->flat = cnt < P.flat_below * n ? 1 : 0;
           h->remote = (FUSED && s != P.r) ? 1 : 0;
           h->slice_id = slice_id;
           h->slice_bags = slice_bags;
@@ -559,17 +662,64 @@ __global__ void __launch_bounds__(288, TMA ? 1 : 4)
       const unsigned wpay = pay + 4u * (unsigned)P.payload_cap;
       const uint4* tab = t < kMaxSmemTables ? s_tab[t]
                                             : reinterpret_cast<const uint4*>(P.tables[t]);
-      for (int b = group; b < nb; b += ngroups) {
-        float acc[NV][EPU];
-        const int lo = so[b] - base, hi = so[b + 1] - base;
-        if constexpr (TMA) {
-          if (staged)
+      // a5: bag b of this stage goes to row (row0 + b) of s's [b_s][G*D], column block
+      // g = toff + t (fused), or to staging row (j0 + b), table t (pool)
+      float* dst0;
+      long long stride;
+      if (FUSED) {
+        dst0 = h->out_base + ((long long)h->row0 * P.G + (P.toff + t)) * D;
+        stride = (long long)P.G * D;
+      } else {
+        dst0 = h->out_base + (h->j0 * P.T + t) * (long long)D;
+        stride = (long long)P.T * D;
+      }
+      if (TMA && staged) {
+        for (int b = group; b < nb; b += ngroups) {
+          float acc[NV][EPU];
+          const int lo = so[b] - base, hi = so[b + 1] - base;
+          if constexpr (TMA)
             pool_bag_smem<LPB, NV>(pay, P.DU, P.box4, (unsigned)P.ncb * cb_stride(P.box4), lo,
                                    hi, lane, acc);
+          if (P.mean && hi > lo) {   // R#27: IEEE binary32 division by the bag length
+            const float L = (float)(hi - lo);
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+              for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
+          }
+          float* dst = dst0 + (long long)b * stride;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
+            const int c = lane + v * LPB;
+            if (c < P.DU) {
+#pragma unroll
+              for (int e = 0; e < EPU; e += 4)
+                st_out4(dst + EPU * c + e,
+                        make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+            }
+          }
+        }
+      } else if (h->flat) {
+        // short bags: contiguous block of bags per lane group, rows walked across bag
+        // boundaries so U rows stay in flight
+        const int q = nb / ngroups, rmd = nb - q * ngroups;
+        const int b0 = group * q + (group < rmd ? group : rmd);
+        const int b1 = b0 + q + (group < rmd ? 1 : 0);
+        if (b0 < b1) {
+          if (staged)
+            pool_run_lsu<ELEM, LPB, NV, UF, true, WEIGHTED>(tab, P.DU, pay, nullptr, wpay, nullptr,
+                                                            so, base, b0, b1, lane, P.mean != 0,
+                                                            dst0, stride);
           else
-            pool_bag_lsu<ELEM, LPB, NV, U, false, false>(tab, P.DU, 0u, P.indices + base, 0u,
-                                                         nullptr, lo, hi, lane, acc);
-        } else {
+            pool_run_lsu<ELEM, LPB, NV, UF, false, WEIGHTED>(
+                tab, P.DU, 0u, P.indices + base, 0u, WEIGHTED ? P.weights + base : nullptr, so,
+                base, b0, b1, lane, P.mean != 0, dst0, stride);
+        }
+      } else {
+        // long bags: one bag per lane group at a time, round robin, U rows in flight
+        for (int b = group; b < nb; b += ngroups) {
+          float acc[NV][EPU];
+          const int lo = so[b] - base, hi = so[b + 1] - base;
           if (staged)
             pool_bag_lsu<ELEM, LPB, NV, U, true, WEIGHTED>(tab, P.DU, pay, nullptr, wpay,
                                                            nullptr, lo, hi, lane, acc);
@@ -577,27 +727,23 @@ __global__ void __launch_bounds__(288, TMA ? 1 : 4)
             pool_bag_lsu<ELEM, LPB, NV, U, false, WEIGHTED>(
                 tab, P.DU, 0u, P.indices + base, 0u, WEIGHTED ? P.weights + base : nullptr, lo,
                 hi, lane, acc);
-        }
-        if (P.mean && hi > lo) {   // R#27: IEEE binary32 division by the bag length
-          const float L = (float)(hi - lo);
+          if (P.mean && hi > lo) {   // R#27: IEEE binary32 division by the bag length
+            const float L = (float)(hi - lo);
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
+            for (int v = 0; v < NV; ++v)
 #pragma unroll
-            for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
-        }
-        float* dst;
-        if (FUSED)   // a5: row (row0 + b) of s's [b_s][G*D], column block g = toff + t
-          dst = h->out_base + ((long long)(h->row0 + b) * P.G + (P.toff + t)) * D;
-        else         // staging [B][T][D] by global row: block of s starts at p_s*T*D
-          dst = h->out_base + ((h->j0 + b) * P.T + t) * (long long)D;
+              for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
+          }
+          float* dst = dst0 + (long long)b * stride;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
-          const int c = lane + v * LPB;
-          if (c < P.DU) {
+          for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
+            const int c = lane + v * LPB;
+            if (c < P.DU) {
 #pragma unroll
-            for (int e = 0; e < EPU; e += 4)
-              st_out4(dst + EPU * c + e,
-                      make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+              for (int e = 0; e < EPU; e += 4)
+                st_out4(dst + EPU * c + e,
+                        make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+            }
           }
         }
       }

@@ -83,8 +83,8 @@ struct emb_a2a {
   // options
   int64_t S = 32, order = 0, threads = 256, timeout_ms = 10000, validate = 0, unroll = 0;
   int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, tma = 0;
-  int64_t stage_kb = 32, vec = 0, pdl = 1;
-  int64_t chunk = 16;
+  int64_t stage_kb = 32, vec = 0, pdl = 1, flat_below = 12;
+  int64_t chunk = 32;
   int64_t trace_cap = 0;                 // records; 0 = tracing off
   unsigned long long* d_trace = nullptr;
 
@@ -270,6 +270,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.slice_cnt = h->d_slice_cnt;
   P.nstages = (int)h->stages;
   P.pdl = (int)h->pdl;
+  P.flat_below = (int)h->flat_below;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
   stage_layout(P, (int)h->stage_kb, (int)h->idx_cap);
@@ -785,6 +786,9 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
   } else if (k == "idx_cap") {
     if (v < 0 || v > 16384) return fail(h, EMB_A2A_EINVAL, "idx_cap in [0, 16384]");
     h->idx_cap = v;
+  } else if (k == "flat_below") {
+    if (v < 0 || v > 1 << 20) return fail(h, EMB_A2A_EINVAL, "flat_below >= 0");
+    h->flat_below = v;
   } else if (k == "pdl") {
     h->pdl = v ? 1 : 0;
   } else if (k == "vec") {
@@ -838,6 +842,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "tma") *v = h->tma;
   else if (k == "vec") *v = h->vec;
   else if (k == "pdl") *v = h->pdl;
+  else if (k == "flat_below") *v = h->flat_below;
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
   else if (k == "debug_delay_ns") *v = h->delay_ns;

@@ -91,7 +91,7 @@ def test_random_configs_vs_oracle(seed):
     g.destroy()
 
 
-@pytest.mark.parametrize("tma,vec", [(0, 0), (1, 0), (0, 2), (0, 4)])
+@pytest.mark.parametrize("tma,vec", [(0, 0), (1, 0), (0, 2), (0, 4), (0, 8)])
 @pytest.mark.parametrize("D", [4, 8, 12, 16, 60, 64, 92, 128, 132, 256, 384, 512, 1024])
 def test_all_lane_mappings(D, tma, vec):
     """Every lane mapping (LPB 1..32, NV 1..8) incl. masked columns (D/4 not a power of 2)."""
@@ -120,7 +120,8 @@ def test_all_lane_mappings(D, tma, vec):
     {"stages": 2}, {"stages": 8}, {"ctas_per_sm": 1}, {"idx_cap": 0}, {"idx_cap": 5},
     {"idx_cap": 64}, {"threads": 64, "chunk": 5}, {"tma": 1}, {"tma": 1, "stage_kb": 1},
     {"tma": 1, "stage_kb": 3}, {"tma": 1, "stages": 8, "stage_kb": 64}, {"chunk": 1}, {"chunk": 3}, {"chunk": 63},
-    {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32}, {"pdl": 0},
+    {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32}, {"pdl": 0}, {"flat_below": 0}, {"flat_below": 1000},
+    {"flat_below": 1000, "vec": 2}, {"flat_below": 1000, "idx_cap": 4},
 ])
 def test_results_invariant_to_tunables(opts):
     """Slice size, schedule, CTA size, unroll and index staging must not change any bit."""

@@ -82,17 +82,20 @@ def test_half_lane_mappings(dtype, D):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_mean_pooling(seed):
+@pytest.mark.parametrize("flat", [0, 1000])
+def test_mean_pooling(seed, flat):
     p = random_problem(2100 + seed, value_mode=seed % 2, ragged=seed % 3 == 0)
     ref = oracle.emb_a2a(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets,
                          pooling=oracle.MEAN)
-    got = run_gpu(p, [torch.from_numpy(t).to(dev()) for t in p.tables], pooling="mean")
+    got = run_gpu(p, [torch.from_numpy(t).to(dev()) for t in p.tables], pooling="mean",
+                  opts={"flat_below": flat})
     for a, b in zip(got, ref):
         np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("seed", range(6))
-@pytest.mark.parametrize("opts", [{}, {"idx_cap": 3}, {"idx_cap": 0}, {"vec": 2}])
+@pytest.mark.parametrize("opts", [{}, {"idx_cap": 3}, {"idx_cap": 0}, {"vec": 2},
+                                  {"flat_below": 0}, {"flat_below": 1000}])
 def test_per_sample_weights(seed, opts):
     p = random_problem(2200 + seed, value_mode=seed % 2, ragged=seed % 3 == 1)
     w = weights_for(p, seed % 2)
