@@ -1,0 +1,49 @@
+"""Small forwards of every kernel path for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck).  W = 1 by default (the sanitizer serialises kernels, which would stall a cross-rank
+receive wait); --W 2 for memcheck of the loopback protocol.  Each output is checked against the
+oracle, so a sanitizer-induced difference would also show."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+from paper_2305_06942_b200 import LoopbackGroup  # noqa: E402
+from tests._problems import random_problem  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--W", type=int, default=1)
+args = ap.parse_args()
+dev = torch.device("cuda:0")
+cases = [({}, "sum"), ({"tma": 1}, "sum"), ({"flat_below": 1000}, "sum"), ({"vec": 2}, "mean"),
+         ({"idx_cap": 3}, "sum"), ({"tma": 1, "stage_kb": 1}, "sum")]
+n = 0
+for seed, (opts, pooling) in enumerate(cases):
+    p = random_problem(900 + seed, W=args.W, value_mode=1, max_B=64, max_D=64)
+    if args.W > 1:
+        opts = dict(opts, timeout_ms=120000)
+    g = LoopbackGroup(p.W, dev, opts)
+    g.register_tables([[torch.from_numpy(t).to(dev) for t in p.rank_tables(r)] for r in range(p.W)],
+                      p.B, p.part, dim=p.D, pooling=pooling)
+    idx = [torch.from_numpy(i).to(dev) for i in p.indices]
+    off = [torch.from_numpy(o).to(dev) for o in p.offsets]
+    w = None
+    if pooling == "sum" and seed % 2 == 0:
+        w = [torch.ones(i.size, dtype=torch.float32, device=dev) for i in p.indices]
+    for _ in range(2):
+        outs = g.forward(idx, off, weights=w)
+    ref = oracle.emb_a2a(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets,
+                         pooling=oracle.MEAN if pooling == "mean" else oracle.SUM)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o.cpu().numpy(), r), (opts, pooling)
+    for r, h in enumerate(g.handles):   # the unfused pool kernel too
+        send = torch.zeros((p.B, p.T[r], p.D), device=dev)
+        h.pool_local(idx[r], off[r], send)
+    torch.cuda.synchronize()
+    g.destroy()
+    n += 1
+print(f"sanitize_smoke: {n} cases OK (W={args.W})")
