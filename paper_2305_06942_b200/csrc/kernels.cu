@@ -163,8 +163,10 @@ void stage_layout(KParams& P, int kb, int idx_cap) {
     P.payload_cap = groups * 4;
     payload = groups * gbytes;
   } else {
-    P.payload_cap = idx_cap;
-    payload = (idx_cap * 4 * (P.weights ? 2 : 1) + 127) / 128 * 128;
+    // weighted: indices and weights share the same payload bytes (half the entries each), so
+    // the stage -- and the CTAs per SM -- stay the same size
+    P.payload_cap = P.weights ? (idx_cap + 1) / 2 : idx_cap;
+    payload = (idx_cap * 4 + 127) / 128 * 128 + (P.weights ? 128 : 0);
   }
   P.stage_bytes = P.payload_off + payload;
 }
