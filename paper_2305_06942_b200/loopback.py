@@ -38,12 +38,20 @@ class LoopbackGroup:
                                                             pooling, dtype), self.W)
 
     def forward(self, indices: Sequence[torch.Tensor], offsets: Sequence[torch.Tensor],
-                sync: bool = True, weights: Optional[Sequence[torch.Tensor]] = None
-                ) -> List[torch.Tensor]:
+                sync: bool = True, weights: Optional[Sequence[torch.Tensor]] = None,
+                aligned: bool = False) -> List[torch.Tensor]:
+        """aligned: put a cross-rank device barrier in front of the W forwards so the virtual
+        ranks start together (the host issues them one after another)."""
         cur = torch.cuda.current_stream(self.device)
         outs = []
+        if aligned:   # hold the GPU long enough for the host to enqueue all W forwards
+            torch.cuda._sleep(4_000_000)
         for r, h in enumerate(self.handles):
             self.streams[r].wait_stream(cur)
+        if aligned:
+            for r, h in enumerate(self.handles):
+                h.device_barrier(self.streams[r])
+        for r, h in enumerate(self.handles):
             outs.append(h.forward(indices[r], offsets[r], stream=self.streams[r],
                                   per_sample_weights=None if weights is None else weights[r]))
         for s in self.streams:
