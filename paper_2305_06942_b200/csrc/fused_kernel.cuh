@@ -445,14 +445,18 @@ static_assert(sizeof(StageHdr) <= kHdrBytes, "stage header too large");
 //                      group moves on to the next stage while slow ones finish ("make forward
 //                      progress after setting WG_Done instead of waiting on an inter-WG barrier",
 //                      P:151).
+// Register budget of the LDG path: 4 CTAs/SM (<= 56 regs) when a lane holds one 16-byte unit per
+// row, 3 CTAs/SM (<= 75 regs) when it holds several (wide rows: 16 units in flight per lane
+// would spill at 56 registers).  Measured round 1: DLRM-small (NV=1) 16.4 vs 20.2 us with 3;
+// DLRM-wide (NV=2) 222 vs 250 us with 4.
 #ifndef EMBA2A_LSU_MINB
-#define EMBA2A_LSU_MINB 4
+#define EMBA2A_LSU_MINB(NV) ((NV) >= 2 ? 3 : 4)
 #endif
 #ifndef EMBA2A_LSU_UNITS
 #define EMBA2A_LSU_UNITS 16
 #endif
 template <int ELEM, int LPB, int NV, bool FUSED, bool TMA, bool WEIGHTED>
-__global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB)
+__global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
     emb_a2a_kernel(const __grid_constant__ KParams P) {
   static_assert(!TMA || (ELEM == 0 && !WEIGHTED), "TMA gather: fp32 unweighted tables only");
   constexpr int EPU = Elem<ELEM>::EPU;
