@@ -72,6 +72,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_bf16_to_float.argtypes = [ctypes.c_uint16]
         L.oracle_f16_to_float.restype = ctypes.c_float
         L.oracle_f16_to_float.argtypes = [ctypes.c_uint16]
+        L.oracle_backward_sgd.restype = I32
+        L.oracle_backward_sgd.argtypes = [I32, P, I32, I64, P, P, P, P, P, P, P, I32, P,
+                                          ctypes.c_float]
         L.oracle_slice_plan.restype = I32
         L.oracle_slice_plan.argtypes = [I32, I32, P, I32, I64, I32, P, I64, P]
         L.oracle_signal_count.restype = I64
@@ -193,6 +196,30 @@ def emb_a2a_rows(seed: int, mode: int, part: Sequence[int], D: int, B: int, T: S
     if rc:
         raise OracleError(rc, "emb_a2a_rows")
     return out[: sel.size]
+
+
+def backward_sgd(part: Sequence[int], D: int, B: int, T: Sequence[int],
+                 tables: Sequence[np.ndarray], indices: Sequence[np.ndarray],
+                 offsets: Sequence[np.ndarray], grad: Sequence[np.ndarray], lr: float,
+                 weights: Optional[Sequence[np.ndarray]] = None, pooling: int = SUM
+                 ) -> List[np.ndarray]:
+    """Backward + SGD (f3): returns updated copies of the G fp32 tables.  grad[s] is destination
+    rank s's pooled-output gradient [b_s, G*D] (the forward output's layout)."""
+    W = len(T)
+    p, Ta, idx, off, nnz = _common(part, T, indices, offsets)
+    tabs = [np.array(t, dtype=np.float32, copy=True, order="C") for t in tables]
+    rows = np.array([t.shape[0] for t in tabs], dtype=np.int64)
+    grads = [np.ascontiguousarray(x, dtype=np.float32) for x in grad]
+    grads = [x if x.size else np.zeros(1, np.float32) for x in grads]
+    wk, warr = _weights(weights, idx)
+    keep = [_ptr_array(tabs), _ptr_array(idx), _ptr_array(off), _ptr_array(grads)]
+    rc = lib().oracle_backward_sgd(W, _ptr(p), D, B, _ptr(Ta), _ptr(keep[0]), _ptr(rows),
+                                   _ptr(keep[1]), _ptr(keep[2]),
+                                   _ptr(warr) if warr is not None else None, _ptr(nnz), pooling,
+                                   _ptr(keep[3]), lr)
+    if rc:
+        raise OracleError(rc, "backward_sgd")
+    return tabs
 
 
 def slice_plan(r: int, W: int, part: Sequence[int], T_r: int, S: int, order: int = 0) -> np.ndarray:

@@ -309,6 +309,69 @@ int oracle_emb_a2a_rows(uint64_t seed, int mode, int W, const int64_t* part, int
 }
 
 /* ------------------------------------------------------------------------------------------
+ * Backward + SGD update (the paper's future work): the DP -> MP
+ * All-to-All of the pooled-output gradient and the embedding-gradient scatter/update.
+ * For every global table g (owner r, local t) and row x:
+ *     acc = +0;  for k ascending over table t's positions in indices_r with indices_r[k] == x:
+ *         j = bag of k (offsets_r[t*B + j] <= k < offsets_r[t*B + j + 1]), s = dest(j), i = j - p_s
+ *         c = grad_s[i][g*D + d]            (sum)
+ *         c = fl(w_k * grad_s[i][g*D + d])  (weighted)          R#26
+ *         c = fl(grad_s[i][g*D + d] / L_j)  (mean)              R#27
+ *         acc = fl(acc + c)
+ *     if x occurs at all:  W_g[x][d] = fl(W_g[x][d] - fl(lr * acc))          R#29
+ * tables: G fp32 arrays, updated in place.  grad: W per-destination arrays [b_s][G*D] fp32.
+ * Plain and slow: for every row, a scan over all of the table's positions.
+ * ---------------------------------------------------------------------------------------- */
+int oracle_backward_sgd(int W, const int64_t* part, int D, int64_t B, const int32_t* T,
+                        float* const* tables, const int64_t* rows,
+                        const int32_t* const* indices, const int32_t* const* offsets,
+                        const float* const* weights, const int64_t* nnz, int pooling,
+                        const float* const* grad, float lr) {
+    int rc = validate(W, part, B, T, rows, indices, offsets, nnz);
+    if (rc) return rc;
+    if (weights && pooling != ORACLE_SUM) return ORACLE_EINVAL;
+    int64_t G = 0;
+    for (int r = 0; r < W; ++r) G += T[r];
+    float* acc = (float*)malloc(sizeof(float) * (D > 0 ? D : 1));
+    if (!acc) return ORACLE_EINVAL;
+    int64_t g = 0;
+    for (int r = 0; r < W; ++r) {
+        for (int t = 0; t < T[r]; ++t, ++g) {
+            const int32_t* off = offsets[r];
+            const int64_t k0 = off[(int64_t)t * B], k1 = off[(int64_t)(t + 1) * B];
+            for (int64_t x = 0; x < rows[g]; ++x) {
+                int found = 0;
+                for (int d = 0; d < D; ++d) acc[d] = +0.0f;
+                int64_t j = 0;
+                for (int64_t k = k0; k < k1; ++k) {
+                    while (off[(int64_t)t * B + j + 1] <= k) ++j;      /* bag of position k */
+                    if (indices[r][k] != x) continue;
+                    found = 1;
+                    int s;
+                    int64_t i;
+                    oracle_destination(W, part, j, &s, &i);
+                    const float* gr = grad[s] + (i * G + g) * D;
+                    const int64_t L = off[(int64_t)t * B + j + 1] - off[(int64_t)t * B + j];
+                    for (int d = 0; d < D; ++d) {
+                        volatile float c = gr[d];
+                        if (weights) c = weights[r][k] * c;
+                        else if (pooling == ORACLE_MEAN) c = c / (float)L;
+                        acc[d] = acc[d] + c;
+                    }
+                }
+                if (!found) continue;
+                for (int d = 0; d < D; ++d) {
+                    volatile float step = lr * acc[d];
+                    tables[g][x * D + d] = tables[g][x * D + d] - step;
+                }
+            }
+        }
+    }
+    free(acc);
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------------------------
  * Slice plan of rank r (row a1).  P:147: communication happens per *slice* of S output vectors;
  * "the slice index along with the global batch size and node count can then be used to
  * determine if the slice needs to be communicated remotely"; slices never cross a
