@@ -139,6 +139,50 @@ int emb_a2a_pool_local_weighted(emb_a2a_t* h, const int32_t* indices, const int3
                                 const float* weights, int64_t num_indices, void* stream,
                                 float* send);
 
+/* ---------------------------------------------------------------- backward
+ * The paper leaves the backward pass to future work (Sec 5 "explore ... the backward
+ * pass").  What it computes (R#29-R#31; oracle_backward_sgd): rank s holds
+ * dL/d(out_s), [b_s][G*D] float32, the gradient of its forward output.  The owner r of table g
+ * (local t) applies, for every row x that occurs in g's bags,
+ *     W_g[x] = W_g[x] - fl(lr * sum_{k : idx_k = x} c_k)
+ *     c_k = grad_s[j - p_s][g*D .. g*D + D)   for lookup k in bag j, s = dest(j)
+ *           (fl(w_k * grad) with per-sample weights, fl(grad / L_j) with mean pooling)
+ * i.e. the forward's All-to-All reversed (data parallel -> model parallel) followed by the
+ * embedding-gradient segment reduction and a sparse SGD step.  Rows that do not occur are not
+ * touched.  fp32 tables only (EINVAL otherwise).  The sum over a row's lookups is taken in a
+ * fixed, deterministic order (runs of C sorted lookups, then runs in order, R#31), so
+ * repeated calls give bitwise-identical tables; it matches the oracle's ascending-order sum
+ * within the fp32 rounding bound, and bitwise when every partial sum is exact. */
+
+/* Backward plan (not collective): sorts this rank's lookups by (local table, row) on `stream`
+ * (stable LSD radix sort in the library's kernels).  Depends only on the forward's inputs, so it
+ * can run as soon as they are known (e.g. on a side stream overlapping the dense layers).
+ *  indices, offsets  as for emb_a2a_forward (DEVICE, borrowed: offsets must stay valid until
+ *                    the backward that uses this plan has run, for mean pooling).
+ *  weights           DEVICE float32[num_indices] per-sample weights, or NULL (sum pooling only).
+ * Plan storage is library-owned and grow-only; a new plan replaces the previous one.
+ * EINVAL if the sort key t << ceil(log2(max rows)) | row needs more than 32 bits. */
+int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                          const float* weights, int64_t num_indices, void* stream);
+
+/* Fused backward (collective), asynchronous on `stream`, using the last plan.
+ *  grad   DEVICE float32 [b_r][G*D] row-major (the forward output's layout): dL/d(out_r).
+ *         Borrowed until the stream passes the op.  16-byte aligned.
+ *  lr     SGD learning rate.
+ * One kernel: every CTA pushes its share of grad's column blocks (owner q's tables) straight
+ * into q's library-owned staging buffer over NVLink and releases q's per-source counter
+ * (red.release.sys), waits for every source's rows (ld.acquire.sys, bounded by timeout_ms ->
+ * ETIMEOUT on the next call), then reduces and updates this rank's tables in place.  The
+ * registered table memory is written: nothing else may read or write it until the stream passes
+ * the op.  Staging is double-buffered by backward epoch, like the forward's receive buffers. */
+int emb_a2a_backward(emb_a2a_t* h, const float* grad, float lr, void* stream);
+
+/* Unfused backward, second half (not collective): the same reduce + update from a caller-owned
+ * DEVICE float32 gradient in model-parallel layout [B][T_r][D] (row j = global sample j) -- what
+ * NCCL all_to_all_single delivers from the destination ranks' [b_s][T_r*D] column blocks.  The
+ * baseline is: pack columns, all_to_all_single, backward_local. */
+int emb_a2a_backward_local(emb_a2a_t* h, const float* grad_mp, float lr, void* stream);
+
 /* Cross-rank device barrier on `stream` (collective; benchmark tooling, not part of the op):
  * returns immediately on the host; the stream proceeds once every rank's barrier kernel has
  * arrived (system-scope release/acquire counters in the symmetric region).  Used to align the
@@ -177,6 +221,9 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  its indices from global memory
  *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
  *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
+ *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 256] (default 128)
+ *   "bwd_share"    divide the backward's persistent grid by this (default 1): W virtual ranks on
+ *                  one GPU must all be resident at once (loopback sets it to W)
  *   "debug_delay_ns"  test knob: CTAs sleep this long before signalling (stress tests)
  *   "debug_skip_signal_to"  test knob: never signal rank v (>= 0), to exercise ETIMEOUT */
 int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t value);
@@ -188,7 +235,9 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* value);
  *   1 mean), "global_batch", "num_slices",
  *   "num_chunks", "chunk_bags" (C),
  *   "expected_in:<src>" (signals rank src sends here per forward), "region_bytes",
- *   "last_grid" (CTAs of the last fused launch), "kernel_launches" (total kernels launched). */
+ *   "last_grid" (CTAs of the last fused launch), "kernel_launches" (total kernels launched),
+ *   "backward_epoch" (fused backwards issued), "plan_lookups" (lookups in the current backward
+ *   plan, -1 = none), "bwd_grid" (CTAs of the backward kernel), "bwd_chunk" (lookups per chunk). */
 int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* value);
 
 /* Introspection for parity tests (synchronous; not on the hot path):

@@ -43,6 +43,9 @@ _SIGS = {
     "emb_a2a_forward_host": (_I, [_P, _P, _P, _I64, _P, _P]),
     "emb_a2a_pool_local": (_I, [_P, _P, _P, _I64, _P, _P]),
     "emb_a2a_pool_local_weighted": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
+    "emb_a2a_backward_plan": (_I, [_P, _P, _P, _P, _I64, _P]),
+    "emb_a2a_backward": (_I, [_P, _P, ctypes.c_float, _P]),
+    "emb_a2a_backward_local": (_I, [_P, _P, ctypes.c_float, _P]),
     "emb_a2a_device_barrier": (_I, [_P, _P]),
     "emb_a2a_set_option": (_I, [_P, ctypes.c_char_p, _I64]),
     "emb_a2a_get_option": (_I, [_P, ctypes.c_char_p, _PI64]),

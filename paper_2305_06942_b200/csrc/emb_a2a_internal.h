@@ -26,6 +26,10 @@ struct DevPeers {
   unsigned long long* flag_out[kMaxW];    // &flags_s[r]: counter r increments in peer s
   long long n_in[kMaxW];                  // signals expected from source q per forward
   unsigned long long* barrier_out[kMaxW]; // peer q's barrier counter (device barrier)
+  // backward (f3): peer q's gradient staging [B][T_q][D] float32 by parity, and our arrival
+  // counter inside peer q's region (rows of our batch block pushed to q)
+  float* gstage[kMaxW][2];
+  unsigned long long* bflag_out[kMaxW];
 };
 
 // Kernel parameters, passed by value (constant bank).  Scalars + the two small tables the
@@ -147,5 +151,77 @@ cudaError_t launch_slice_plan(const KParams& P, int* out, cudaStream_t st);
 cudaError_t launch_validate(const int* indices, const int* offsets, long long nnz, long long TB,
                             long long B, int T, const long long* rows_dev, int* err_dev,
                             cudaStream_t st);
+
+// ------------------------------------------------------------------------------ backward (f3)
+// Sort plan: this rank's lookups as (key = t << rbits | row, payload = bag id t*B + j [, weight])
+// sorted stably by key with an LSD radix sort (8-bit digits, one onesweep pass per digit).
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
+constexpr int kMaxPasses = 4;                          // 32-bit keys
+
+struct SortParams {
+  const int* indices;
+  const int* offsets;
+  const float* weights;        // NULL = unweighted
+  unsigned* keys;              // [n] out (keygen) / pass ping-pong buffers
+  int* bags;
+  float* wts;
+  unsigned* hist;              // [kMaxPasses][256] digit counts (zeroed before keygen)
+  long long TB, B;
+  int rbits, passes;
+};
+
+struct PassParams {
+  const unsigned* keys_in;
+  unsigned* keys_out;
+  const int* bags_in;
+  int* bags_out;
+  const float* wts_in;         // NULL = no weight payload
+  float* wts_out;
+  const unsigned* hist;        // this pass's 256 digit counts
+  unsigned long long* status;  // [ntiles][256] look-back words of this pass
+  unsigned* tile_ctr;          // this pass's tile ticket (zeroed before keygen)
+  long long n;
+  int shift;
+  unsigned stamp;              // plan number (30 bits): stale look-back words are ignored
+};
+
+// The fused backward (exchange + reduce + update) and the unfused reduce share one kernel.
+struct BwdParams {
+  const float* grad;           // fused: own [b_r][G*D] output gradient; local: [B][T][D] (MP)
+  float* stage;                // fused: own staging [B][T][D] for this parity (remote rows)
+  const DevPeers* peers;
+  unsigned long long* bflags_in;   // own backward arrival counters, src * kFlagStride
+  const unsigned* keys;        // sorted plan
+  const int* bags;
+  const float* wts;            // sorted weights (weighted plan) or NULL
+  const int* offsets;          // bag lengths for mean pooling
+  float* const* tables;        // device array of T fp32 table pointers (updated in place)
+  float* scratch;              // [nchunks][D] partial sums of segments that cross chunks
+  unsigned long long* chunk_flag;  // [nchunks] = stamp when scratch[c] is published
+  int* err;
+  long long n;                 // lookups in the plan
+  long long B, timeout_ns;
+  unsigned long long bepoch;   // 1-based fused-backward number (exchange counters, parity)
+  unsigned long long stamp;    // 1-based reduce-launch number (chunk flags)
+  float lr;
+  int W, r, T, D, G, toff, C, nchunks, rbits, fused, mean, parity;
+  long long part[kMaxW + 1];
+  int allT[kMaxW];
+  int tofs[kMaxW];
+};
+
+cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int npasses,
+                             long long ntiles, int grid_keygen, cudaStream_t st);
+cudaError_t plan_backward(const BwdParams& P, int threads, int share, unsigned* grid,
+                          size_t* smem);
+cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size_t smem,
+                            cudaStream_t st);
+// chunk size (lookups per warp work unit) for dimension D
+inline int bwd_chunk(int D) {
+  int c = 2048 / D;
+  return c > 32 ? 32 : (c < 1 ? 1 : c);
+}
 
 }  // namespace emba2a

@@ -122,6 +122,31 @@ struct emb_a2a {
   LaunchPlan plan_fused[2], plan_pool[2]; // cached launch configurations [weighted]
                                           // (fn == nullptr: stale)
   int64_t kernel_launches = 0;
+
+  // backward (f3)
+  int64_t bwd_threads = 128, bwd_share = 1;
+  uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
+  uint64_t rstamp = 0;                   // reduce launches (chunk-flag stamps)
+  uint32_t plan_no = 0;                  // sort plans (look-back stamps)
+  unsigned long long* bflags = nullptr;  // own backward arrival counters
+  float* gstage[2] = {nullptr, nullptr}; // own gradient staging [B][T][D] by parity
+  unsigned* d_keys[2] = {nullptr, nullptr};
+  int* d_bags[2] = {nullptr, nullptr};
+  float* d_wts[2] = {nullptr, nullptr};
+  size_t plan_cap = 0, wts_cap = 0;
+  unsigned* d_hist = nullptr;            // [kMaxPasses][256] + kMaxPasses tile tickets
+  unsigned long long* d_status = nullptr;
+  size_t status_cap = 0;
+  float* d_scratch = nullptr;
+  unsigned long long* d_cflag = nullptr;
+  size_t chunk_cap = 0;
+  bool planned = false, plan_weighted = false;
+  int64_t plan_n = 0;
+  int plan_buf = 0, rbits = 0;
+  const int32_t* plan_offsets = nullptr;
+  int bwd_mode = -1;                     // cached launch: mode it was planned for
+  unsigned bwd_grid = 0;
+  size_t bwd_smem = 0;
 };
 
 namespace {
@@ -154,11 +179,14 @@ int check_async(emb_a2a* h) {
   if (h->h_err && *(volatile int*)h->h_err != 0) {
     const int v = *(volatile int*)h->h_err;
     h->poisoned = true;
-    return fail(h, EMB_A2A_ETIMEOUT,
-                (v & 0x200) ? "device barrier timed out on rank %d (code %d, timeout_ms=%lld)"
-                            : "receive wait timed out: rank %d never received all slices from "
-                              "rank %d (timeout_ms=%lld)",
-                h->rank, v & 0xff, (long long)h->timeout_ms);
+    const char* what =
+        (v & 0x800) ? "backward chunk fold timed out on rank %d (code %d, timeout_ms=%lld)"
+        : (v & 0x400) ? "backward exchange wait timed out: rank %d never received all gradient "
+                        "rows from rank %d (timeout_ms=%lld)"
+        : (v & 0x200) ? "device barrier timed out on rank %d (code %d, timeout_ms=%lld)"
+                      : "receive wait timed out: rank %d never received all slices from "
+                        "rank %d (timeout_ms=%lld)";
+    return fail(h, EMB_A2A_ETIMEOUT, what, h->rank, v & 0xff, (long long)h->timeout_ms);
   }
   return EMB_A2A_OK;
 }
@@ -179,6 +207,28 @@ void release_registration(emb_a2a* h) {
   h->d_slice_cnt = nullptr;
   if (h->d_idx_stage) cudaFree(h->d_idx_stage);
   if (h->d_off_stage) cudaFree(h->d_off_stage);
+  for (int x = 0; x < 2; ++x) {
+    if (h->d_keys[x]) cudaFree(h->d_keys[x]);
+    if (h->d_bags[x]) cudaFree(h->d_bags[x]);
+    if (h->d_wts[x]) cudaFree(h->d_wts[x]);
+    h->d_keys[x] = nullptr;
+    h->d_bags[x] = nullptr;
+    h->d_wts[x] = nullptr;
+    h->gstage[x] = nullptr;
+  }
+  h->plan_cap = h->wts_cap = 0;
+  if (h->d_hist) cudaFree(h->d_hist);
+  if (h->d_status) cudaFree(h->d_status);
+  if (h->d_scratch) cudaFree(h->d_scratch);
+  if (h->d_cflag) cudaFree(h->d_cflag);
+  h->d_hist = nullptr;
+  h->d_status = nullptr;
+  h->d_scratch = nullptr;
+  h->d_cflag = nullptr;
+  h->status_cap = h->chunk_cap = 0;
+  h->planned = false;
+  h->bwd_mode = -1;
+  h->bflags = nullptr;
   h->region = nullptr;
   h->d_peers = nullptr;
   h->d_tables = nullptr;
@@ -501,16 +551,26 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   }
   h->rows.assign(rows, rows + num_local_tables);
 
-  // ---- symmetric region: [arrival counters W x 128 B | barrier counter 128 B | recv0 | recv1],
-  //      256-B aligned pieces
-  const size_t flag_bytes = ((size_t)(h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
+  // ---- symmetric region: [forward arrival counters W x 128 B | barrier counter 128 B |
+  //      backward arrival counters W x 128 B | recv0 | recv1 | gstage0 | gstage1], 256-B aligned
+  //      pieces.  gstage (backward, fp32 tables only): [B][T_r][D] float32 gradient rows pushed
+  //      by their data-parallel owners.
+  const size_t flag_bytes = ((size_t)(2 * h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
   const size_t buf_bytes = ((size_t)h->b * G * dim * 4 + 255) / 256 * 256;
-  h->region_bytes = flag_bytes + 2 * std::max<size_t>(buf_bytes, 256);
+  auto gstage_bytes = [&](int Tq) -> size_t {
+    if (table_dtype != EMB_A2A_F32) return 256;
+    return std::max<size_t>(((size_t)Tq * global_batch * dim * 4 + 255) / 256 * 256, 256);
+  };
+  const size_t gsz = gstage_bytes(num_local_tables);
+  h->region_bytes = flag_bytes + 2 * std::max<size_t>(buf_bytes, 256) + 2 * gsz;
   CUDA_TRY(h, cudaMalloc((void**)&h->region, h->region_bytes));
   CUDA_TRY(h, cudaMemset(h->region, 0, h->region_bytes));
   h->flags = (unsigned long long*)h->region;
+  h->bflags = h->flags + (size_t)(h->W + 1) * kFlagStride;
   h->recv[0] = (float*)(h->region + flag_bytes);
   h->recv[1] = (float*)(h->region + flag_bytes + std::max<size_t>(buf_bytes, 256));
+  h->gstage[0] = (float*)(h->region + flag_bytes + 2 * std::max<size_t>(buf_bytes, 256));
+  h->gstage[1] = (float*)((char*)h->gstage[0] + gsz);
 
   Handles mine;
   memset(&mine, 0, sizeof(mine));
@@ -560,6 +620,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
     h->host_peers.recv[q][1] = (float*)(base + fq + bufq);
     h->host_peers.flag_out[q] = (unsigned long long*)(base) + (size_t)h->rank * kFlagStride;
     h->host_peers.barrier_out[q] = (unsigned long long*)(base) + (size_t)h->W * kFlagStride;
+    h->host_peers.bflag_out[q] =
+        (unsigned long long*)(base) + (size_t)(h->W + 1 + h->rank) * kFlagStride;
+    h->host_peers.gstage[q][0] = (float*)(base + fq + 2 * bufq);
+    h->host_peers.gstage[q][1] = (float*)(base + fq + 2 * bufq + gstage_bytes(all[q].T));
   }
 
   // ---- device-side tables, plan, counters
@@ -588,6 +652,9 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   CUDA_TRY(h, cudaDeviceSynchronize());
   h->epoch = 0;
   h->barrier_epoch = 0;
+  h->bepoch = 0;
+  h->planned = false;
+  h->bwd_mode = -1;
   for (int w = 0; w < 2; ++w) {
     h->plan_fused[w] = LaunchPlan();
     h->plan_pool[w] = LaunchPlan();
@@ -734,6 +801,235 @@ int emb_a2a_pool_local_weighted(emb_a2a_t* h, const int32_t* indices, const int3
   return EMB_A2A_OK;
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ backward (f3)
+namespace {
+
+int ceil_log2(int64_t v) {   // bits needed for values 0 .. v-1
+  int b = 0;
+  while (b < 63 && ((int64_t)1 << b) < v) ++b;
+  return b;
+}
+
+template <typename T>
+int grow(emb_a2a* h, T** p, size_t n) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  CUDA_TRY(h, cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)));
+  return EMB_A2A_OK;
+}
+
+BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
+  BwdParams P;
+  memset(&P, 0, sizeof(P));
+  P.grad = grad;
+  P.peers = h->d_peers;
+  P.bflags_in = h->bflags;
+  P.keys = h->d_keys[h->plan_buf];
+  P.bags = h->d_bags[h->plan_buf];
+  P.wts = h->plan_weighted ? h->d_wts[h->plan_buf] : nullptr;
+  P.offsets = h->plan_offsets;
+  P.tables = (float* const*)h->d_tables;
+  P.scratch = h->d_scratch;
+  P.chunk_flag = h->d_cflag;
+  P.err = h->d_err;
+  P.n = h->planned ? h->plan_n : 0;
+  P.B = h->B;
+  P.timeout_ns = (long long)h->timeout_ms * 1000000ll;
+  P.lr = lr;
+  P.W = h->W;
+  P.r = h->rank;
+  P.T = h->T;
+  P.D = h->D;
+  P.G = h->G;
+  P.toff = h->toff;
+  P.C = bwd_chunk(h->D);
+  P.nchunks = (int)((P.n + P.C - 1) / P.C);
+  P.rbits = h->rbits;
+  P.fused = fused;
+  P.mean = h->mean;
+  int acc = 0;
+  for (int q = 0; q < h->W; ++q) {
+    P.allT[q] = h->allT[q];
+    P.tofs[q] = acc;
+    acc += h->allT[q];
+  }
+  for (int s = 0; s <= h->W; ++s) P.part[s] = h->part[s];
+  return P;
+}
+
+int run_backward(emb_a2a* h, BwdParams& P, cudaStream_t st) {
+  const int mode = P.wts ? 1 : (P.mean ? 2 : 0);
+  if (h->bwd_mode != mode) {
+    cudaError_t e = plan_backward(P, (int)h->bwd_threads, (int)h->bwd_share, &h->bwd_grid,
+                                  &h->bwd_smem);
+    if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "backward plan: %s", cudaGetErrorString(e));
+    h->bwd_mode = mode;
+  }
+  h->rstamp += 1;
+  P.stamp = h->rstamp;
+  cudaError_t e = launch_backward(P, h->bwd_grid, (int)h->bwd_threads, h->bwd_smem, st);
+  if (e != cudaSuccess) {
+    h->poisoned = true;
+    return fail(h, EMB_A2A_ECUDA, "backward kernel launch: %s", cudaGetErrorString(e));
+  }
+  h->kernel_launches++;
+  return EMB_A2A_OK;
+}
+
+int bwd_common_checks(emb_a2a* h, const char* what) {
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "%s before register_tables", what);
+  if (h->elem != EMB_A2A_F32)
+    return fail(h, EMB_A2A_EINVAL, "%s: backward updates fp32 tables only (R#30)", what);
+  return EMB_A2A_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
+                          const float* weights, int64_t num_indices, void* stream) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = bwd_common_checks(h, "backward_plan");
+  if (rc) return rc;
+  if (num_indices < 0 || num_indices >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "num_indices out of range (int32 CSR, R#8)");
+  if ((h->T > 0 && h->B > 0) && (!offsets || (num_indices > 0 && !indices)))
+    return fail(h, EMB_A2A_EINVAL, "indices/offsets are NULL");
+  if (weights && h->mean)
+    return fail(h, EMB_A2A_EINVAL, "per-sample weights need sum pooling (R#26)");
+  int64_t rmax = 1;
+  for (int t = 0; t < h->T; ++t) rmax = std::max<int64_t>(rmax, h->rows[t]);
+  const int tbits = ceil_log2(std::max(1, h->T)), rbits = ceil_log2(rmax);
+  if (tbits + rbits > 32)
+    return fail(h, EMB_A2A_EINVAL, "backward sort key needs %d bits (> 32): T_r * max rows too "
+                "large", tbits + rbits);
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->validate && h->T > 0 && h->B > 0) {
+    rc = run_validate(h, indices, offsets, num_indices, st);
+    if (rc) return rc;
+  }
+  const int64_t n = (h->T > 0) ? num_indices : 0;
+  const int passes = (tbits + rbits + 7) / 8;
+  const int C = bwd_chunk(h->D);
+  const int64_t nchunks = (n + C - 1) / C;
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  const bool wtd = weights != nullptr && n > 0;
+  // plan storage (grow-only)
+  if ((size_t)n > h->plan_cap) {
+    for (int x = 0; x < 2; ++x) {
+      if ((rc = grow(h, &h->d_keys[x], n))) return rc;
+      if ((rc = grow(h, &h->d_bags[x], n))) return rc;
+    }
+    h->plan_cap = n;
+  }
+  if (wtd && (size_t)n > h->wts_cap) {
+    for (int x = 0; x < 2; ++x)
+      if ((rc = grow(h, &h->d_wts[x], n))) return rc;
+    h->wts_cap = n;
+  }
+  if (!h->d_hist && (rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses))) return rc;
+  const size_t nstatus = (size_t)passes * ntiles * 256;
+  if (nstatus > h->status_cap) {
+    if ((rc = grow(h, &h->d_status, nstatus))) return rc;
+    CUDA_TRY(h, cudaMemset(h->d_status, 0, nstatus * 8));
+    h->status_cap = nstatus;
+  }
+  if ((size_t)nchunks > h->chunk_cap) {
+    if ((rc = grow(h, &h->d_scratch, (size_t)nchunks * h->D))) return rc;
+    if ((rc = grow(h, &h->d_cflag, nchunks))) return rc;
+    CUDA_TRY(h, cudaMemset(h->d_cflag, 0, (size_t)nchunks * 8));
+    h->chunk_cap = nchunks;
+  }
+  h->plan_no += 1;
+  h->rbits = rbits;
+  h->plan_weighted = wtd;
+  h->plan_offsets = offsets;
+  h->plan_n = n;
+  h->plan_buf = passes & 1;
+  h->planned = true;
+  if (n == 0) return EMB_A2A_OK;
+  CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (kMaxPasses * 256 + kMaxPasses) * sizeof(unsigned), st));
+  SortParams S;
+  memset(&S, 0, sizeof(S));
+  S.indices = indices;
+  S.offsets = offsets;
+  S.weights = wtd ? weights : nullptr;
+  S.keys = h->d_keys[0];
+  S.bags = h->d_bags[0];
+  S.wts = h->d_wts[0];
+  S.hist = h->d_hist;
+  S.TB = (long long)h->T * h->B;
+  S.B = h->B;
+  S.rbits = rbits;
+  S.passes = passes;
+  PassParams pp[kMaxPasses];
+  for (int p = 0; p < passes; ++p) {
+    PassParams& q = pp[p];
+    memset(&q, 0, sizeof(q));
+    q.keys_in = h->d_keys[p & 1];
+    q.keys_out = h->d_keys[(p + 1) & 1];
+    q.bags_in = h->d_bags[p & 1];
+    q.bags_out = h->d_bags[(p + 1) & 1];
+    q.wts_in = wtd ? h->d_wts[p & 1] : nullptr;
+    q.wts_out = wtd ? h->d_wts[(p + 1) & 1] : nullptr;
+    q.hist = h->d_hist + p * 256;
+    q.status = h->d_status + (size_t)p * ntiles * 256;
+    q.tile_ctr = h->d_hist + kMaxPasses * 256 + p;
+    q.n = n;
+    q.shift = 8 * p;
+    q.stamp = h->plan_no;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long TB = (long long)h->T * h->B;
+  const long long gk = std::min<long long>((TB + 255) / 256, (long long)sms * 8);
+  cudaError_t e = launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1), st);
+  if (e != cudaSuccess) {
+    h->planned = false;
+    return fail(h, EMB_A2A_ECUDA, "backward plan launch: %s", cudaGetErrorString(e));
+  }
+  h->kernel_launches += 1 + passes;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_backward(emb_a2a_t* h, const float* grad, float lr, void* stream) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = bwd_common_checks(h, "backward");
+  if (rc) return rc;
+  if (h->T > 0 && !h->planned)
+    return fail(h, EMB_A2A_ESTATE, "backward before backward_plan");
+  if (!grad && h->b > 0) return fail(h, EMB_A2A_EINVAL, "grad is NULL");
+  if (grad && ((uintptr_t)grad % 16)) return fail(h, EMB_A2A_EINVAL, "grad must be 16-B aligned");
+  DeviceGuard guard(h->dev);
+  h->bepoch += 1;
+  BwdParams P = bwd_params(h, grad, lr, 1);
+  P.parity = (int)(h->bepoch & 1);
+  P.stage = h->gstage[P.parity];
+  P.bepoch = h->bepoch;
+  return run_backward(h, P, (cudaStream_t)stream);
+}
+
+int emb_a2a_backward_local(emb_a2a_t* h, const float* grad_mp, float lr, void* stream) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = bwd_common_checks(h, "backward_local");
+  if (rc) return rc;
+  if (h->T == 0) return EMB_A2A_OK;
+  if (!h->planned) return fail(h, EMB_A2A_ESTATE, "backward_local before backward_plan");
+  if (!grad_mp && h->B > 0) return fail(h, EMB_A2A_EINVAL, "grad_mp is NULL");
+  if (grad_mp && ((uintptr_t)grad_mp % 16))
+    return fail(h, EMB_A2A_EINVAL, "grad_mp must be 16-B aligned");
+  DeviceGuard guard(h->dev);
+  BwdParams P = bwd_params(h, grad_mp, lr, 0);
+  return run_backward(h, P, (cudaStream_t)stream);
+}
+
 int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
   if (!h) return EMB_A2A_EINVAL;
   int rc = check_async(h);
@@ -817,6 +1113,14 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
       CUDA_TRY(h, cudaMemset(h->d_trace, 0, (size_t)(2 + 2 * v) * 8));
       h->trace_cap = v;
     }
+  } else if (k == "bwd_threads") {
+    if (v < 32 || v > 256 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..256, x32");
+    h->bwd_threads = v;
+    h->bwd_mode = -1;
+  } else if (k == "bwd_share") {
+    if (v < 1 || v > kMaxW) return fail(h, EMB_A2A_EINVAL, "bwd_share in [1, %d]", kMaxW);
+    h->bwd_share = v;
+    h->bwd_mode = -1;
   } else if (k == "debug_delay_ns") {
     h->delay_ns = std::max<int64_t>(0, v);
   } else if (k == "debug_skip_signal_to") {
@@ -845,6 +1149,8 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "flat_below") *v = h->flat_below;
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
+  else if (k == "bwd_threads") *v = h->bwd_threads;
+  else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;
   else if (k == "debug_skip_signal_to") *v = h->skip_to;
   else return EMB_A2A_EINVAL;
@@ -873,6 +1179,10 @@ int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "chunk_bags") *v = h->C;
   else if (k == "region_bytes") *v = (int64_t)h->region_bytes;
   else if (k == "last_grid") *v = h->last_grid;
+  else if (k == "backward_epoch") *v = (int64_t)h->bepoch;
+  else if (k == "plan_lookups") *v = h->planned ? h->plan_n : -1;
+  else if (k == "bwd_grid") *v = h->bwd_grid;
+  else if (k == "bwd_chunk") *v = bwd_chunk(h->D);
   else if (k.rfind("expected_in:", 0) == 0) {
     const int q = atoi(k.c_str() + 12);
     if (q < 0 || q >= h->W) return EMB_A2A_EINVAL;

@@ -219,6 +219,42 @@ class EmbA2A:
                                       _stream_ptr(stream, self.device), out.data_ptr())
         self._err(rc, "emb_a2a_forward_host")
 
+    # -------------------------------------------------------------- backward (f3)
+    def backward_plan(self, indices: torch.Tensor, offsets: torch.Tensor, stream=None,
+                      per_sample_weights: Optional[torch.Tensor] = None) -> None:
+        """Sort this rank's lookups by (table, row) for the next backward (not collective).
+        offsets must stay alive until that backward has run (mean pooling reads bag lengths)."""
+        _check_dev_tensor(offsets, torch.int32, "offsets", self.device)
+        _check_dev_tensor(indices, torch.int32, "indices", self.device)
+        n = indices.numel()
+        w = None
+        if per_sample_weights is not None:
+            _check_dev_tensor(per_sample_weights, torch.float32, "per_sample_weights", self.device)
+            if per_sample_weights.numel() != n:
+                raise ValueError("per_sample_weights must align with indices")
+            w = per_sample_weights.data_ptr() if n else None
+        self._plan_refs = (indices, offsets, per_sample_weights)
+        rc = lib.emb_a2a_backward_plan(self._h, indices.data_ptr() if n else None,
+                                       offsets.data_ptr(), w, n, _stream_ptr(stream, self.device))
+        self._err(rc, "emb_a2a_backward_plan")
+
+    def backward(self, grad: torch.Tensor, lr: float, stream=None) -> None:
+        """Fused backward (collective): grad = dL/d(out) [b_r, G*D] float32 on this device; the
+        registered tables are updated in place (sparse SGD, W -= lr * dL/dW)."""
+        _check_dev_tensor(grad, torch.float32, "grad", self.device)
+        if tuple(grad.shape) != (self.b, self.G * self.D):
+            raise ValueError(f"grad must be [{self.b}, {self.G * self.D}]")
+        rc = lib.emb_a2a_backward(self._h, grad.data_ptr() if grad.numel() else None, float(lr),
+                                  _stream_ptr(stream, self.device))
+        self._err(rc, "emb_a2a_backward")
+
+    def backward_local(self, grad_mp: torch.Tensor, lr: float, stream=None) -> None:
+        """Unfused second half: reduce + update from a model-parallel gradient [B, T_r, D]."""
+        _check_dev_tensor(grad_mp, torch.float32, "grad_mp", self.device)
+        rc = lib.emb_a2a_backward_local(self._h, grad_mp.data_ptr() if grad_mp.numel() else None,
+                                        float(lr), _stream_ptr(stream, self.device))
+        self._err(rc, "emb_a2a_backward_local")
+
     def device_barrier(self, stream=None) -> None:
         """Collective: the stream waits on the device until every rank has arrived."""
         self._err(lib.emb_a2a_device_barrier(self._h, _stream_ptr(stream, self.device)),

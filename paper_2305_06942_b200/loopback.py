@@ -60,5 +60,27 @@ class LoopbackGroup:
             torch.cuda.synchronize(self.device)
         return outs
 
+    def backward(self, indices: Sequence[torch.Tensor], offsets: Sequence[torch.Tensor],
+                 grads: Sequence[torch.Tensor], lr: float, sync: bool = True,
+                 weights: Optional[Sequence[torch.Tensor]] = None, plan: bool = True) -> None:
+        """Plan (sort) + fused backward on every virtual rank, W streams.  The backward's
+        persistent grid is shared W ways so all W kernels are resident together (each waits for
+        the others' gradient rows)."""
+        cur = torch.cuda.current_stream(self.device)
+        for r, h in enumerate(self.handles):
+            if h.get_option("bwd_share") != self.W:
+                h.set_option("bwd_share", self.W)
+            self.streams[r].wait_stream(cur)
+        if plan:
+            for r, h in enumerate(self.handles):
+                h.backward_plan(indices[r], offsets[r], stream=self.streams[r],
+                                per_sample_weights=None if weights is None else weights[r])
+        for r, h in enumerate(self.handles):
+            h.backward(grads[r], lr, stream=self.streams[r])
+        for s in self.streams:
+            cur.wait_stream(s)
+        if sync:
+            torch.cuda.synchronize(self.device)
+
     def destroy(self):
         run_ranks(lambda r: self.handles[r].destroy(), self.W)

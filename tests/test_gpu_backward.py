@@ -1,0 +1,291 @@
+"""GPU parity of the backward: sort plan + fused exchange/reduce/SGD kernel
+through the C ABI, against oracle.backward_sgd, element by element.
+
+Tolerance.  The oracle sums a row's contributions in ascending lookup order (R#29); the kernel
+sums runs of C sorted lookups, then the runs in order (R#31) -- a different rounding order of
+the same sum.  Each side's error is at most gamma_n * S (S = sum of |c_k| for that element,
+computed by the oracle on |grad|, |w|; n = lookups of that row), so the gate is
+    |gpu - oracle| <= 2 * gamma_n * |lr| * S + 2u * (|W_new| + |lr * acc|)      (u = 2^-24)
+(the last term covers the two sides rounding fl(lr * acc) and W - step independently).  In
+exact-integer mode every partial sum is exact, so the result must be bitwise equal.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests._problems import Problem, csr_from_bags, from_config, random_problem
+from tests.test_oracle_backward import grads_for
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -24
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+class Run:
+    """Loopback group with this problem's tables on the device (updated in place)."""
+
+    def __init__(self, p: Problem, pooling="sum", opts=None):
+        from paper_2305_06942_b200 import LoopbackGroup
+        self.p = p
+        self.g = LoopbackGroup(p.W, dev(), opts)
+        self.tabs = [[torch.from_numpy(np.ascontiguousarray(t)).to(dev()) for t in p.rank_tables(r)]
+                     for r in range(p.W)]
+        self.g.register_tables(self.tabs, p.B, p.part, dim=p.D, pooling=pooling)
+        self.idx = [torch.from_numpy(np.ascontiguousarray(i)).to(dev()) for i in p.indices]
+        self.off = [torch.from_numpy(np.ascontiguousarray(o)).to(dev()) for o in p.offsets]
+
+    def backward(self, grads, lr, weights=None, plan=True):
+        gd = [torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(dev()) for x in grads]
+        w = None if weights is None else [torch.from_numpy(x).to(dev()) for x in weights]
+        self.g.backward(self.idx, self.off, gd, lr, weights=w, plan=plan)
+
+    def tables(self):
+        return [t.cpu().numpy() for r in range(self.p.W) for t in self.tabs[r]]
+
+    def forward(self):
+        return [o.cpu().numpy() for o in self.g.forward(self.idx, self.off)]
+
+    def destroy(self):
+        self.g.destroy()
+
+
+def occurrences(p: Problem):
+    """Per global table: count of lookups of each row (n for gamma_n)."""
+    out = []
+    for r in range(p.W):
+        for t in range(p.T[r]):
+            o = p.offsets[r]
+            seg = p.indices[r][o[t * p.B]: o[(t + 1) * p.B]]
+            out.append(np.bincount(seg, minlength=p.tables[p.toff(r) + t].shape[0]))
+    return out
+
+
+def bound_check(p, got, want, grads, lr, weights=None, pooling=oracle.SUM):
+    zero = [np.zeros_like(t) for t in p.tables]
+    absw = None if weights is None else [np.abs(w) for w in weights]
+    S = oracle.backward_sgd(p.part, p.D, p.B, p.T, zero, p.indices, p.offsets,
+                            [np.abs(g) for g in grads], -1.0, weights=absw, pooling=pooling)
+    acc = oracle.backward_sgd(p.part, p.D, p.B, p.T, zero, p.indices, p.offsets, grads, -1.0,
+                              weights=weights, pooling=pooling)
+    for g, (a, b, s, ac, n) in enumerate(zip(got, want, S, acc, occurrences(p))):
+        nn = n[:, None].astype(np.float64)
+        gam = nn * U / (1 - nn * U)
+        tol = 2 * gam * abs(lr) * s.astype(np.float64) + \
+            2 * U * (np.abs(b).astype(np.float64) + abs(lr) * np.abs(ac).astype(np.float64)) + 1e-30
+        err = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        bad = err > tol
+        assert not bad.any(), (g, np.argwhere(bad)[:5], err[bad][:5], tol[bad][:5])
+        untouched = n == 0
+        np.testing.assert_array_equal(a[untouched], p.tables[g][untouched])
+
+
+# ------------------------------------------------------------------------------- exact mode
+
+@pytest.mark.parametrize("seed", range(8))
+def test_backward_exact_int_bitwise(seed):
+    """Integer tables and gradients, lr = -1 / 0.5: every sum is exact -> bitwise equal."""
+    p = random_problem(5000 + seed, value_mode=1, ragged=seed % 2 == 1, max_B=128, max_D=64)
+    grads = grads_for(p, seed, 1)
+    lr = -1.0 if seed % 2 == 0 else 0.5
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, lr)
+    run = Run(p)
+    run.backward(grads, lr)
+    got = run.tables()
+    run.destroy()
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_tiny_config_backward_exact():
+    cfg = synth.config_for("tiny", value_mode=1)
+    p = from_config(cfg)
+    grads = grads_for(p, 7, 1)
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 0.25)
+    run = Run(p)
+    run.backward(grads, 0.25)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+# ------------------------------------------------------------------------------- fp32 mode
+
+@pytest.mark.parametrize("seed", range(8))
+def test_backward_fp32_within_rounding_bound(seed):
+    p = random_problem(5100 + seed, value_mode=0, ragged=seed % 3 == 1, max_B=128, max_D=128)
+    grads = grads_for(p, seed, 0)
+    lr = 0.05
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, lr)
+    run = Run(p)
+    run.backward(grads, lr)
+    got = run.tables()
+    run.destroy()
+    bound_check(p, got, want, grads, lr)
+
+
+@pytest.mark.parametrize("mode", ["weighted", "mean"])
+def test_backward_variants(mode):
+    p = random_problem(5200, value_mode=0, max_B=128, max_D=64)
+    grads = grads_for(p, 3, 0)
+    weights = pooling = None
+    kw = {}
+    if mode == "weighted":
+        cfg = synth.config_for("tiny")
+        weights = [synth.gen_weights(cfg, r, p.indices[r].size) for r in range(p.W)]
+        kw["weights"] = weights
+        pooling = oracle.SUM
+    else:
+        pooling = oracle.MEAN
+        kw["pooling"] = oracle.MEAN
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 0.1, **kw)
+    run = Run(p, pooling="mean" if mode == "mean" else "sum")
+    run.backward(grads, 0.1, weights=weights)
+    got = run.tables()
+    run.destroy()
+    bound_check(p, got, want, grads, 0.1, weights=weights, pooling=pooling)
+
+
+@pytest.mark.parametrize("D", [4, 64, 256, 1024])
+def test_hot_row_spanning_many_chunks(D):
+    """One row looked up thousands of times (a Zipf head): its run crosses hundreds of chunks
+    and more than one 32-chunk look-back window; exact-int grads -> bitwise."""
+    B, W = 256, 2
+    rng = np.random.default_rng(D)
+    bags = [[[5] * 12 + list(rng.integers(0, 40, 3)) for _ in range(B)]]
+    i, o = csr_from_bags(bags)
+    tab = rng.integers(-8, 8, (40, D)).astype(np.float32)
+    tab2 = rng.integers(-8, 8, (40, D)).astype(np.float32)
+    i2, o2 = csr_from_bags([[[7] * 3 for _ in range(B)]])
+    p = Problem(W, [1, 1], D, B, synth.even_partition(B, W), [tab, tab2], [i, i2], [o, o2])
+    grads = grads_for(p, 1, 1)
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 1.0)
+    run = Run(p)
+    run.backward(grads, 1.0)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+def test_deterministic_and_fused_equals_local():
+    """Two identical backwards give bitwise-identical tables; the unfused backward_local from the
+    model-parallel gradient layout gives the same bits as the fused exchange."""
+    p = random_problem(5300, W=4, value_mode=0, max_B=128, max_D=64)
+    grads = grads_for(p, 5, 0)
+    res = []
+    for _ in range(2):
+        run = Run(p)
+        run.backward(grads, 0.03)
+        res.append(run.tables())
+        run.destroy()
+    for a, b in zip(*res):
+        np.testing.assert_array_equal(a, b)
+    # unfused: grad_mp[r] = [B][T_r][D] gathered on the host (the all_to_all's output layout)
+    full = np.concatenate(grads, axis=0).reshape(p.B, p.G, p.D)
+    run = Run(p)
+    for r, h in enumerate(run.g.handles):
+        h.backward_plan(run.idx[r], run.off[r])
+        mp = torch.from_numpy(np.ascontiguousarray(full[:, p.toff(r):p.toff(r) + p.T[r], :])).to(dev())
+        h.backward_local(mp, 0.03)
+    torch.cuda.synchronize()
+    for a, b in zip(run.tables(), res[0]):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+def test_training_steps_forward_backward_interleaved():
+    """forward -> backward -> forward ... over 3 steps on the same handle (exchange epochs, staging
+    parity, chunk stamps, plan reuse); each forward sees the previous step's updated tables."""
+    p = random_problem(5400, W=2, value_mode=1, max_B=64, max_D=32)
+    run = Run(p)
+    tabs = [t.copy() for t in p.tables]
+    for step in range(3):
+        outs = run.forward()
+        ref = oracle.emb_a2a(p.part, p.D, p.B, p.T, tabs, p.indices, p.offsets)
+        for a, b in zip(outs, ref):
+            np.testing.assert_array_equal(a, b)
+        grads = grads_for(p, 10 + step, 1)
+        tabs = oracle.backward_sgd(p.part, p.D, p.B, p.T, tabs, p.indices, p.offsets, grads, 1.0)
+        run.backward(grads, 1.0, plan=(step != 2) or True)
+        for a, b in zip(run.tables(), tabs):
+            np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+def test_empty_plan_and_empty_blocks():
+    """No lookups at all on one rank, a rank with an empty batch block, all-empty bags."""
+    D, B = 8, 6
+    tab = np.arange(10 * D, dtype=np.float32).reshape(10, D)
+    i0, o0 = csr_from_bags([[[1, 2], [], [3], [], [], [1]]])
+    i1, o1 = csr_from_bags([[[] for _ in range(B)]])
+    p = Problem(2, [1, 1], D, B, np.array([0, 0, B]), [tab, tab.copy()], [i0, i1], [o0, o1])
+    grads = [np.zeros((0, 2 * D), np.float32), np.ones((B, 2 * D), np.float32)]
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 1.0)
+    run = Run(p)
+    run.backward(grads, 1.0)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+def test_backward_rejects_half_tables_and_missing_plan():
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    from paper_2305_06942_b200.emb_a2a import EmbA2AError
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    t = torch.zeros(10, 8, device=dev())
+    h.register_tables([t], 4)
+    g = torch.zeros(4, 8, device=dev())
+    with pytest.raises(EmbA2AError):
+        h.backward(g, 1.0)                  # no plan yet
+    h.register_tables([t.to(torch.bfloat16)], 4)
+    with pytest.raises(EmbA2AError):
+        h.backward_plan(torch.zeros(4, dtype=torch.int32, device=dev()),
+                        torch.arange(5, dtype=torch.int32, device=dev()))
+    h.destroy()
+
+
+@pytest.mark.parametrize("name", ["dlrm_small"])
+def test_full_size_backward_sampled_rows(name):
+    """BASELINE config at full size (W=1 per-rank work, as bench.py times it): the plan sorts
+    every lookup; check the updated table on sampled rows against the oracle on just the
+    lookups of those rows (the sum over a row depends only on that row's lookups)."""
+    cfg = synth.config_for(name, W=1)
+    csr = synth.gen_all_csr(cfg, 0)
+    idx_h, off_h = csr[0]
+    rng = np.random.default_rng(0)
+    grad = (rng.integers(-(1 << 20), 1 << 20, (cfg.B, cfg.G * cfg.D)) * 2.0 ** -20).astype(np.float32)
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    tabs = [torch.zeros(cfg.R, cfg.D, device=dev()) for _ in range(cfg.T[0])]
+    h.register_tables(tabs, cfg.B)
+    idx = torch.from_numpy(idx_h).to(dev())
+    off = torch.from_numpy(off_h).to(dev())
+    h.backward_plan(idx, off)
+    h.backward(torch.from_numpy(grad).to(dev()), -1.0)     # zero tables, lr=-1: table = dL/dW
+    torch.cuda.synchronize()
+    for t in (0, cfg.T[0] - 1):
+        o = off_h[t * cfg.B:(t + 1) * cfg.B + 1]
+        seg = idx_h[o[0]:o[-1]]
+        uniq, cnt = np.unique(seg, return_counts=True)
+        pick = np.concatenate([uniq[np.argsort(-cnt)[:4]], rng.choice(uniq, 12, replace=False)])
+        got = tabs[t][torch.from_numpy(pick.astype(np.int64)).to(dev())].cpu().numpy()
+        # oracle on the sub-problem of just these rows (remapped to 0..len(pick)-1)
+        bags = []
+        for j in range(cfg.B):
+            rows = seg[o[j] - o[0]:o[j + 1] - o[0]]
+            bags.append([int(np.nonzero(pick == x)[0][0]) for x in rows if x in set(pick.tolist())])
+        si, so = csr_from_bags([bags])
+        sub_grad = [grad[:, t * cfg.D:(t + 1) * cfg.D]]
+        want = oracle.backward_sgd([0, cfg.B], cfg.D, cfg.B, [1], [np.zeros((len(pick), cfg.D), np.float32)],
+                                   [si], [so], sub_grad, -1.0)[0]
+        S = oracle.backward_sgd([0, cfg.B], cfg.D, cfg.B, [1], [np.zeros((len(pick), cfg.D), np.float32)],
+                                [si], [so], [np.abs(sub_grad[0])], -1.0)[0]
+        n = np.array([np.sum(seg == x) for x in pick], np.float64)[:, None]
+        tol = 2 * (n * U / (1 - n * U)) * S + 4 * U * np.abs(want) + 1e-30
+        assert np.all(np.abs(got.astype(np.float64) - want) <= tol), t
+    h.destroy()
