@@ -50,6 +50,7 @@ def parse():
                          "working set exceeds L2; flushed: L2 flush + per-step events")
     ap.add_argument("--no-baseline", action="store_true", help="skip the unfused NCCL baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--no-backward", action="store_true", help="skip the f3 backward timing")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
     return ap.parse_args()
@@ -428,6 +429,11 @@ def main():
                    "fused_speedup_vs_permute": un_p_ms / ms_step,
                    "fused_equals_unfused_bitwise": same}
 
+    backward = None
+    if not args.no_backward:
+        backward = backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared,
+                                    b2b_loop, max_over_ranks, peak_hbm, peak_src)
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, [c for c in csr_batches if c is not None], args.cpu_seconds)
@@ -457,6 +463,7 @@ def main():
                    "max over ranks"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
         "flushed": flushed, "clocks": clocks, "gpu_launches": int(launches),
+        "backward": backward,
     }
     if shared:
         line["test_mode"] = "EMBA2A_SHARED_GPU=1: all ranks on one GPU; not a bench value"
@@ -469,6 +476,79 @@ def main():
     h.destroy()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b_loop,
+                     max_over_ranks, peak_hbm, peak_src):
+    """f3: one training-step backward = sort plan of the batch's lookups + the
+    fused backward kernel (gradient exchange DP -> MP over peer memory, segment reduce, sparse
+    SGD on the tables).  Baseline: pack the owners' column blocks, NCCL all_to_all_single, then
+    the same reduce (backward_local).  Both are timed back to back over the rotating batches;
+    the tables are updated in place (lr tiny) and restored before the parity check."""
+    import torch
+    import torch.distributed as dist
+    T, D, b = cfg.T[rank], cfg.D, h.b
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    grad = torch.randn((b, h.G * D), generator=gen, device=dev, dtype=torch.float32)
+    lr = 1e-6
+    plan_step = lambda k: h.backward_plan(d_in[k][0], d_in[k][1], stream)  # noqa: E731
+
+    def fused_step(k):
+        h.backward_plan(d_in[k][0], d_in[k][1], stream)
+        h.backward(grad, lr, stream)
+
+    send = torch.empty((N, b, T * D), dtype=torch.float32, device=dev)
+    recv = torch.empty((cfg.B, T * D), dtype=torch.float32, device=dev)
+
+    def unfused_step(k):
+        h.backward_plan(d_in[k][0], d_in[k][1], stream)
+        send.copy_(grad.view(b, N, T * D).permute(1, 0, 2))      # owners' column blocks
+        if shared:
+            r_cpu = torch.empty(recv.numel(), dtype=recv.dtype)
+            dist.all_to_all_single(r_cpu, send.view(-1).cpu())
+            recv.view(-1).copy_(r_cpu)
+        else:
+            dist.all_to_all_single(recv.view(-1), send.view(-1))
+        h.backward_local(recv, lr, stream)
+
+    K, W = args.steps, args.warmup
+    l0 = h.query("kernel_launches")
+    step_ms = max_over_ranks(b2b_loop(fused_step, K, W)) / K
+    launches = (h.query("kernel_launches") - l0) // (K + W)
+    plan_ms = max_over_ranks(b2b_loop(plan_step, K, W)) / K
+    h.backward_plan(d_in[0][0], d_in[0][1], stream)
+    kern_ms = max_over_ranks(b2b_loop(lambda k: h.backward(grad, lr, stream), K, W)) / K
+    un_ms = max_over_ranks(b2b_loop(unfused_step, K, W)) / K
+    # parity: fused vs unfused from the same tables on batch 0 (bitwise: same plan, same order)
+    snap = [t.clone() for t in h._tables]
+    fused_step(0)
+    after_f = [t.clone() for t in h._tables]
+    for t, s0 in zip(h._tables, snap):
+        t.copy_(s0)
+    unfused_step(0)
+    torch.cuda.synchronize()
+    same = all(bool(torch.equal(a, t)) for a, t in zip(after_f, h._tables))
+    # algorithmic bytes of the backward kernel (per launch, batch 0): gradient rows read once
+    # (B * T_r * D * 4 at the owner + the pushed share), the sorted lookup list (key + bag,
+    # 8 B per lookup), each distinct (table, row) read and written once
+    idx, off = mine[0]
+    uniq = sum(np.unique(idx[off[t * cfg.B]:off[(t + 1) * cfg.B]]).size for t in range(T))
+    tx = (cfg.B - b) * T * D * 4 if N > 1 else 0
+    alg = cfg.B * T * D * 4 + idx.size * 8 + 2 * uniq * D * 4 + b * (h.G - T) * D * 4 * (N > 1)
+    kern_s = kern_ms / 1e3
+    return {"what": "plan (radix sort by table,row) + fused backward (DP->MP gradient exchange, "
+                    "segment reduce, sparse SGD) per step",
+            "us_per_step": step_ms * 1e3, "us_plan": plan_ms * 1e3, "us_kernel": kern_ms * 1e3,
+            "lookups_per_s": float(np.mean([m[0].size for m in mine])) * N / (step_ms / 1e3),
+            "unfused_us_per_step": un_ms * 1e3,
+            "unfused": "plan + pack column blocks + NCCL all_to_all_single + backward_local",
+            "fused_speedup": un_ms / step_ms, "fused_equals_unfused_bitwise": same,
+            "gpu_launches_per_step": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "bwd_kernel", "achieved": alg / kern_s / 1e9,
+                         "peak": peak_hbm, "unit": "GB/s", "peak_source": peak_src,
+                         "frac": alg / kern_s / 1e9 / peak_hbm, "algorithmic_bytes": int(alg),
+                         "distinct_rows": int(uniq), "nvlink_tx_bytes": int(tx)}}
 
 
 def working_set_mb(cfg, idx, off):

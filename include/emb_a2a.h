@@ -256,6 +256,12 @@ int emb_a2a_read_trace(emb_a2a_t* h, uint64_t* out, int64_t capacity, int64_t* n
  * still writing, unmaps peers, frees the region.  h is invalid afterwards. */
 int emb_a2a_destroy(emb_a2a_t* h);
 
+/* Poll the asynchronous error word (not collective, no GPU work): EMB_A2A_ETIMEOUT if a receive
+ * wait / backward exchange wait / barrier timed out since the last check (the handle is then
+ * poisoned), EMB_A2A_ESTATE if it already was, else OK.  Synchronise the stream first to see
+ * the failures of work enqueued on it. */
+int emb_a2a_check(emb_a2a_t* h);
+
 const char* emb_a2a_last_error(const emb_a2a_t* h);
 const char* emb_a2a_status_string(int status);
 int emb_a2a_abi_version(void);

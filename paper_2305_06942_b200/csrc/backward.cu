@@ -22,10 +22,13 @@
 //                        red.release.sys; then waits (ld.acquire.sys) for every source's rows;
 //                        then reduces: the sorted lookups are cut into chunks of C; a warp
 //                        gathers a chunk's gradient rows and the table rows it will update into
-//                        shared memory (cp.async), sums each run of equal keys in order, and
-//                        updates the row.  A run that crosses chunks is published as a partial
-//                        sum per chunk and folded, in chunk order, by the chunk where it ends
-//                        (the last-finisher pattern of P:149/P:176, made deterministic).
+//                        shared memory (cp.async), sums each run of equal keys in order (lane
+//                        groups take different runs when a row needs fewer than 32 lanes), and
+//                        updates the row.  A run that crosses chunks leaves one partial sum per
+//                        chunk it touches and counts it on the run's counter; whichever chunk
+//                        completes the count folds the partials in chunk order and updates the
+//                        row (the last-finisher pattern of P:149/P:176, with a fixed fold order,
+//                        so the result does not depend on who finishes last).  No warp waits.
 //                        (local) the same reduce from a caller-owned [B][T][D] gradient -- the
 //                        unfused baseline's second half after NCCL all_to_all_single.
 #include "fused_kernel.cuh"
@@ -40,17 +43,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 __device__ __forceinline__ void st_f4(float* p, const float4& v) {
   asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -59,23 +53,42 @@ __device__ __forceinline__ void st_f4(float* p, const float4& v) {
 }
 
 // ------------------------------------------------------------------------------ sort plan
-// Keys of this rank's lookups and the digit histograms of every pass.  One thread per bag.
+// Keys of this rank's lookups and the digit histograms of every pass.  A warp takes 8
+// consecutive bags; their lookups are one contiguous range, walked 32 positions at a time
+// (coalesced), each position's bag found by a 3-step binary search over the 8 bag starts.
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
+  constexpr int BPW = 8;
   __shared__ unsigned h[kMaxPasses * 256];
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) h[i] = 0u;
   __syncthreads();
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long bag = blockIdx.x * (long long)blockDim.x + threadIdx.x; bag < S.TB;
-       bag += stride) {
-    const unsigned t = (unsigned)(bag / S.B);
-    const int lo = S.offsets[bag], hi = S.offsets[bag + 1];
-    for (int k = lo; k < hi; ++k) {
-      const unsigned key = (S.rbits >= 32 ? 0u : (t << S.rbits)) | (unsigned)S.indices[k];
-      S.keys[k] = key;
-      S.bags[k] = (int)bag;
-      if (WEIGHTED) S.wts[k] = S.weights[k];
-      for (int p = 0; p < S.passes; ++p) atomicAdd(&h[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
+  const int lane = threadIdx.x & 31;
+  const long long ngroups = (S.TB + BPW - 1) / BPW;
+  const long long nwt = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; grp < ngroups;
+       grp += nwt) {
+    const long long b0 = grp * BPW;
+    const int nb = (S.TB - b0) < BPW ? (int)(S.TB - b0) : BPW;
+    const int my_off = lane < nb ? S.offsets[b0 + lane] : 0x7fffffff;
+    const int lo = __shfl_sync(kFull, my_off, 0);
+    const int hi = S.offsets[b0 + nb];
+    for (int base = lo; base < hi; base += 32) {
+      const int p = base + lane;
+      int i = 0;
+#pragma unroll
+      for (int step = BPW / 2; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(kFull, my_off, i + step);
+        if (i + step < nb && v <= p) i += step;
+      }
+      if (p < hi) {
+        const long long bag = b0 + i;
+        const unsigned t = (unsigned)(bag / S.B);
+        const unsigned key = (S.rbits >= 32 ? 0u : (t << S.rbits)) | (unsigned)S.indices[p];
+        S.keys[p] = key;
+        S.bags[p] = (int)bag;
+        if (WEIGHTED) S.wts[p] = S.weights[p];
+        for (int q = 0; q < S.passes; ++q) atomicAdd(&h[q * 256 + ((key >> (8 * q)) & 255u)], 1u);
+      }
     }
   }
   __syncthreads();
@@ -198,14 +211,25 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
 }
 
 // ------------------------------------------------------------------------- fused backward
-// MODE 0 sum, 1 weighted (c = fl(w * g), R#26), 2 mean (c = fl(g / L), R#27).  NVC = float4
-// columns per lane (D / 128 rounded up to 1, 2, 4, 8).
+// Sparse SGD step on 4 elements (R#29): w = fl(w - fl(lr * g)).
+__device__ __forceinline__ void sgd4(float4& w, float lr, const float4& g) {
+  w.x = __fsub_rn(w.x, __fmul_rn(lr, g.x));
+  w.y = __fsub_rn(w.y, __fmul_rn(lr, g.y));
+  w.z = __fsub_rn(w.z, __fmul_rn(lr, g.z));
+  w.w = __fsub_rn(w.w, __fmul_rn(lr, g.w));
+}
+
+__device__ __forceinline__ void st_shared_f4(float* p, const float4& v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
 template <int NVC, int MODE>
-__global__ void __launch_bounds__(128) bwd_kernel(const __grid_constant__ BwdParams P) {
+__global__ void __launch_bounds__(128, NVC >= 8 ? 1 : 4) bwd_kernel(const __grid_constant__ BwdParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_pushed[kMaxW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int D = P.D, DU = D >> 2, C = P.C;
+  const int D = P.D, DU = D >> 2;
 
   // ---- exchange (fused, W > 1): push this rank's gradient rows to their table owners
   if (P.fused && P.W > 1) {
@@ -269,24 +293,65 @@ __global__ void __launch_bounds__(128) bwd_kernel(const __grid_constant__ BwdPar
   }
   if (P.T == 0 || P.n == 0) return;
 
-  // ---- reduce + update: warp-level work units (chunks of C sorted lookups)
-  const size_t wbytes = (size_t)2 * C * D * 4 + 32 * 4 + 32 * 8;
-  unsigned char* wb = smem + warp * wbytes;
-  float* sg = reinterpret_cast<float*>(wb);             // [C][D] gradient rows
-  float* stb = sg + (size_t)C * D;                      // [C][D] table rows (per piece)
-  float* sscal = stb + (size_t)C * D;                   // [C] weight or bag length
-  float** stp = reinterpret_cast<float**>(sscal + 32);  // [C] table row pointers (per piece)
+  // ---- reduce + update, pass 1 (R#31).  Work unit = a chunk of 32 consecutive sorted lookups
+  // per warp.  The chunk's runs (pieces of equal keys) are split into NG contiguous ranges, one
+  // per lane group (LPG lanes cover a row); a group walks its range in sorted order with UF
+  // gradient rows in flight per lane and sums each run in ascending lookup order -- the
+  // row-flattened pooling loop of the forward, with runs for bags.  A run that starts and ends
+  // inside the chunk is finished here: queued (row, sum) in the group's registers and applied
+  // in batches (all table-row loads in flight together).  The chunk's first run, if it began in
+  // an earlier chunk, and its last run, if it goes on into the next, are left as partial sums
+  // in the chunk's two scratch slots for pass 2 (bwd_fold_kernel).
+  constexpr int UF = NVC >= 8 ? 1 : 8 / NVC;
+  constexpr int QN = NVC >= 4 ? 2 : 4;                 // finished-run queue per group
+  int LPG = 1;
+  while (LPG < DU && LPG < 32) LPG <<= 1;
+  const int NG = 32 / LPG, grp = lane / LPG, gl = lane - grp * LPG;
+  const long long* sptr = reinterpret_cast<const long long*>(smem + (size_t)warp * P.wbytes);
+  long long* wsrc = reinterpret_cast<long long*>(smem + (size_t)warp * P.wbytes);   // [32] rows
+  long long* wtab = wsrc + 32;                                                      // [32] table
+  float* wsc = reinterpret_cast<float*>(wtab + 32);                                 // [32] scale
+  (void)sptr;
   const unsigned rmask = P.rbits >= 32 ? 0xffffffffu : ((1u << P.rbits) - 1u);
   const long long gw = (long long)blockIdx.x * nw + warp, nwt = (long long)gridDim.x * nw;
   const long long pr = P.part[P.r];
+  const long long n = P.n;
+  const unsigned* __restrict__ keys = P.keys;
+  float4 qacc[QN][NVC];
+  float* qtab[QN];
+  int nq = 0;
+
+  auto flush = [&]() {                               // this group's queued rows: SGD step
+    float4 w[QN][NVC];
+#pragma unroll
+    for (int f = 0; f < QN; ++f)
+#pragma unroll
+      for (int v = 0; v < NVC; ++v) {
+        const int col = gl + LPG * v;
+        w[f][v] = (f < nq && col < DU) ? __ldcg(reinterpret_cast<const float4*>(qtab[f]) + col)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int f = 0; f < QN; ++f)
+      if (f < nq)
+#pragma unroll
+        for (int v = 0; v < NVC; ++v) {
+          const int col = gl + LPG * v;
+          if (col < DU) {
+            sgd4(w[f][v], P.lr, qacc[f][v]);
+            st_f4(qtab[f] + 4 * col, w[f][v]);
+          }
+        }
+    nq = 0;
+  };
 
   for (long long c = gw; c < P.nchunks; c += nwt) {
-    const long long p0 = c * C;
-    const int len = (int)((P.n - p0) < C ? (P.n - p0) : C);
+    const long long p0 = c * kBwdChunk;
+    const int len = (n - p0) < kBwdChunk ? (int)(n - p0) : kBwdChunk;
     unsigned key = 0u;
     int bag = 0;
     if (lane < len) {
-      key = P.keys[p0 + lane];
+      key = keys[p0 + lane];
       bag = P.bags[p0 + lane];
     }
     const unsigned kup = __shfl_up_sync(kFull, key, 1);
@@ -295,15 +360,14 @@ __global__ void __launch_bounds__(128) bwd_kernel(const __grid_constant__ BwdPar
     const unsigned keyl = __shfl_sync(kFull, key, len - 1);
     int flags = 0;
     if (lane == 0) {
-      if (p0 > 0 && P.keys[p0 - 1] == key0) flags |= 1;              // run continues in
-      if (p0 + len < P.n && P.keys[p0 + len] == keyl) flags |= 2;    // run continues out
+      if (p0 > 0 && keys[p0 - 1] == key0) flags |= 1;              // first run continues in
+      if (p0 + len < n && keys[p0 + len] == keyl) flags |= 2;       // last run continues out
     }
     flags = __shfl_sync(kFull, flags, 0);
     const bool cont_in = flags & 1, cont_out = flags & 2;
     const int npieces = __popc(startm);
-
-    // this lane's lookup: where its gradient row lives, its scalar, the piece's table row
-    unsigned long long srow = 0ull;
+    // per lookup: where its gradient row lives, its scalar, the row it updates
+    __syncwarp();                                    // previous chunk's readers are done
     if (lane < len) {
       const int t = (int)(bag / P.B);
       const long long j = bag - (long long)t * P.B;
@@ -315,143 +379,148 @@ __global__ void __launch_bounds__(128) bwd_kernel(const __grid_constant__ BwdPar
                          : P.stage + (j * P.T + t) * D;
       else
         src = P.grad + (j * P.T + t) * D;
-      srow = reinterpret_cast<unsigned long long>(src);
-      if (MODE == 1) sscal[lane] = P.wts[p0 + lane];
-      if (MODE == 2) sscal[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
-      if ((startm >> lane) & 1u) {
-        const int pi = __popc(startm & ((1u << lane) - 1u));
-        const bool fin_here = !(pi == npieces - 1 && cont_out);
-        stp[pi] = fin_here ? P.tables[t] + (size_t)(key & rmask) * D : nullptr;
+      wsrc[lane] = reinterpret_cast<long long>(src);
+      wtab[lane] = reinterpret_cast<long long>(
+          (P.rbits >= 32) ? P.tables[0] + (size_t)key * D
+                          : P.tables[(int)(key >> P.rbits)] + (size_t)(key & rmask) * D);
+      if (MODE == 1) wsc[lane] = P.wts[p0 + lane];
+      if (MODE == 2) wsc[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
+      if (lane == 0) {
+        const bool inside = npieces == 1 && cont_in && cont_out;    // one run covers the chunk
+        P.info[c] = (unsigned char)((cont_out && !inside ? 1 : 0) | (inside ? 2 : 0));
       }
     }
     __syncwarp();
-    // gather the chunk's gradient rows and the table rows it finalises (cp.async, L2 only)
-    const int tot = len * DU;
-    for (int b = 0; b < tot; b += 32) {
-      const int idx = b + lane;
-      const int o = idx < tot ? idx / DU : len - 1;
-      const float* rp = reinterpret_cast<const float*>(__shfl_sync(kFull, srow, o));
-      if (idx < tot) {
-        const int u = idx - o * DU;
-        cp_async16_cg(smem_u32(sg + o * D + 4 * u), rp + 4 * u);
-      }
-    }
-    const int ttot = npieces * DU;
-    for (int idx = lane; idx < ttot; idx += 32) {
-      const int pi = idx / DU, u = idx - pi * DU;
-      const float* tp = stp[pi];
-      if (tp) cp_async16_cg(smem_u32(stb + pi * D + 4 * u), tp + 4 * u);
-    }
-    cp_async_wait_all();
-    __syncwarp();
-
-    float4 acc[NVC];
-#pragma unroll
-    for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int pi = 0;
-    for (int o = 0; o < len; ++o) {
-      float sc = 1.f;
-      if (MODE != 0) sc = sscal[o];
-#pragma unroll
-      for (int v = 0; v < NVC; ++v) {
-        const int u = lane + 32 * v;
-        if (u < DU) {
-          float4 g = lds_f4(smem_u32(sg + o * D + 4 * u));
-          if (MODE == 1) {
-            g.x = __fmul_rn(sc, g.x); g.y = __fmul_rn(sc, g.y);
-            g.z = __fmul_rn(sc, g.z); g.w = __fmul_rn(sc, g.w);
-          } else if (MODE == 2) {
-            g.x = __fdiv_rn(g.x, sc); g.y = __fdiv_rn(g.y, sc);
-            g.z = __fdiv_rn(g.z, sc); g.w = __fdiv_rn(g.w, sc);
-          }
-          add4(acc[v], g);
-        }
-      }
-      const bool end = (o == len - 1) || ((startm >> (o + 1)) & 1u);
-      if (!end) continue;
-      if (pi == npieces - 1 && cont_out) {
-        // partial of a run that continues in the next chunk: publish it for the fold
-#pragma unroll
-        for (int v = 0; v < NVC; ++v) {
-          const int u = lane + 32 * v;
-          if (u < DU) st_f4(P.scratch + c * D + 4 * u, acc[v]);
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_gpu(P.chunk_flag + c, P.stamp);
-      } else {
-        if (pi == 0 && cont_in) {
-          // the run started in an earlier chunk: find that chunk c0 (look back over chunk
-          // starts, 32 at a time), then fold the published partials of c0 .. c-1 in order
-          long long cc = c - 1, c0 = -1;
-          while (c0 < 0) {
-            const long long q = cc - lane;
-            bool starts = false;
-            if (q >= 0)
-              starts = (q == 0) || P.keys[q * C] != key0 || P.keys[q * C - 1] != key0;
-            const unsigned m = __ballot_sync(kFull, starts);
-            if (m) c0 = cc - (__ffs(m) - 1);
-            else cc -= 32;
-          }
-          float4 tot4[NVC];
-#pragma unroll
-          for (int v = 0; v < NVC; ++v) tot4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-          constexpr int BATCH = 8 / NVC;
-          for (long long q0 = c0; q0 < c; q0 += BATCH) {
-            const int nb = (c - q0) < BATCH ? (int)(c - q0) : BATCH;
-            if (lane < nb) {
-              const unsigned long long t0 = globaltimer();
-              while (ld_acquire_gpu(P.chunk_flag + q0 + lane) != P.stamp) {
-                if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
-                  atomicExch(P.err, 0x800);
-                  break;
-                }
-              }
-            }
-            __syncwarp();
-            float4 pv[BATCH][NVC];
-#pragma unroll
-            for (int x = 0; x < BATCH; ++x)
-#pragma unroll
-              for (int v = 0; v < NVC; ++v) {
-                const int u = lane + 32 * v;
-                pv[x][v] = (x < nb && u < DU)
-                               ? __ldcg(reinterpret_cast<const float4*>(P.scratch +
-                                                                        (q0 + x) * D) + u)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-#pragma unroll
-            for (int x = 0; x < BATCH; ++x)
-              if (x < nb)
-#pragma unroll
-                for (int v = 0; v < NVC; ++v) add4(tot4[v], pv[x][v]);
-          }
-#pragma unroll
-          for (int v = 0; v < NVC; ++v) {
-            add4(tot4[v], acc[v]);
-            acc[v] = tot4[v];
-          }
-        }
-        // sparse SGD step on the row (R#29): W = W - fl(lr * g)
-        float* tp = stp[pi];
-#pragma unroll
-        for (int v = 0; v < NVC; ++v) {
-          const int u = lane + 32 * v;
-          if (u < DU) {
-            float4 w = lds_f4(smem_u32(stb + pi * D + 4 * u));
-            w.x = __fsub_rn(w.x, __fmul_rn(P.lr, acc[v].x));
-            w.y = __fsub_rn(w.y, __fmul_rn(P.lr, acc[v].y));
-            w.z = __fsub_rn(w.z, __fmul_rn(P.lr, acc[v].z));
-            w.w = __fsub_rn(w.w, __fmul_rn(P.lr, acc[v].w));
-            st_f4(tp + 4 * u, w);
-          }
-        }
-      }
+    // this group's runs [pa, pb) = positions [lo, hi)
+    const int pa = (npieces * grp) / NG, pb = (npieces * (grp + 1)) / NG;
+    if (pa < pb) {
+      const int lo = __fns(startm, 0, pa + 1);
+      const int hi = pb < npieces ? (int)__fns(startm, 0, pb + 1) : len;
+      int pi = pa;
+      float4 acc[NVC];
 #pragma unroll
       for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      ++pi;
+      for (int q0 = lo; q0 < hi; q0 += UF) {
+        float4 buf[UF][NVC];
+#pragma unroll
+        for (int x = 0; x < UF; ++x) {
+          const int q = q0 + x;
+          const float4* rp = reinterpret_cast<const float4*>(wsrc[q < hi ? q : lo]);
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            const int col = gl + LPG * v;
+            buf[x][v] = (q < hi && col < DU) ? __ldcg(rp + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < UF; ++x) {
+          const int q = q0 + x;
+          if (q >= hi) break;
+          const float s = (MODE != 0) ? wsc[q] : 1.f;
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            float4 cv = buf[x][v];
+            if (MODE == 1) {
+              cv.x = __fmul_rn(s, cv.x); cv.y = __fmul_rn(s, cv.y);
+              cv.z = __fmul_rn(s, cv.z); cv.w = __fmul_rn(s, cv.w);
+            } else if (MODE == 2) {
+              cv.x = __fdiv_rn(cv.x, s); cv.y = __fdiv_rn(cv.y, s);
+              cv.z = __fdiv_rn(cv.z, s); cv.w = __fdiv_rn(cv.w, s);
+            }
+            add4(acc[v], cv);
+          }
+          if (q + 1 < len && !((startm >> (q + 1)) & 1u)) continue;   // run goes on
+          // ---- the run ending at lookup q: finished here, or a partial for pass 2
+          const bool part_in = pi == 0 && cont_in, part_out = pi == npieces - 1 && cont_out;
+          if (part_in || part_out) {
+            float* slot = P.scratch + ((size_t)c * 2 + (part_out ? 1 : 0)) * D;
+#pragma unroll
+            for (int v = 0; v < NVC; ++v) {
+              const int col = gl + LPG * v;
+              if (col < DU) st_f4(slot + 4 * col, acc[v]);
+            }
+          } else {
+#pragma unroll
+            for (int f = 0; f < QN; ++f)
+              if (f == nq) {
+#pragma unroll
+                for (int v = 0; v < NVC; ++v) qacc[f][v] = acc[v];
+                qtab[f] = reinterpret_cast<float*>(wtab[q]);
+              }
+            if (++nq == QN) flush();
+          }
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ++pi;
+        }
+      }
     }
-    __syncwarp();   // the next chunk reuses this warp's shared memory
+  }
+  if (nq > 0) flush();
+}
+
+// ---- reduce + update, pass 2 (R#31): the runs that cross chunk boundaries.  The chunk a run
+// starts in owns it (info bit 0): tot = +0, + its slot-1 partial, + the slot-1 partials of the
+// chunks the run covers entirely (info bit 1, read 32 at a time), + the slot-0 partial of the
+// chunk it ends in -- in chunk order -- then the SGD step on the row.
+template <int NVC>
+__global__ void __launch_bounds__(256) bwd_fold_kernel(const __grid_constant__ BwdParams P) {
+  const int lane = threadIdx.x & 31;
+  const int D = P.D, DU = D >> 2;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned rmask = P.rbits >= 32 ? 0xffffffffu : ((1u << P.rbits) - 1u);
+  constexpr int BATCH = NVC >= 16 ? 1 : 16 / NVC;
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < P.nchunks;
+       c += nw) {
+    if (!(P.info[c] & 1)) continue;
+    const unsigned K = P.keys[c * kBwdChunk + kBwdChunk - 1];
+    float4 tot[NVC];
+#pragma unroll
+    for (int v = 0; v < NVC; ++v) {
+      const int col = lane + 32 * v;
+      tot[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (col < DU)
+        add4(tot[v], __ldcg(reinterpret_cast<const float4*>(P.scratch + (c * 2 + 1) * D) + col));
+    }
+    long long q = c + 1;
+    while (true) {
+      const bool in = q + lane < P.nchunks && (P.info[q + lane] & 2);
+      const unsigned m = __ballot_sync(kFull, in);
+      const int k = (m == kFull) ? 32 : __ffs(~m) - 1;     // chunks q .. q+k-1 lie inside the run
+      for (int x0 = 0; x0 <= k; x0 += BATCH) {             // ... and chunk q+k ends it
+        float4 pv[BATCH][NVC];
+#pragma unroll
+        for (int x = 0; x < BATCH; ++x) {
+          const long long qq = q + x0 + x;
+          const bool ok = x0 + x < k || (x0 + x == k && k < 32);
+          const float* src = P.scratch + (qq * 2 + (x0 + x < k ? 1 : 0)) * D;
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            const int col = lane + 32 * v;
+            pv[x][v] = (ok && col < DU) ? __ldcg(reinterpret_cast<const float4*>(src) + col)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < BATCH; ++x)
+          if (x0 + x < k || (x0 + x == k && k < 32))
+#pragma unroll
+            for (int v = 0; v < NVC; ++v) add4(tot[v], pv[x][v]);
+      }
+      if (k < 32) break;
+      q += 32;
+    }
+    float* tp = (P.rbits >= 32) ? P.tables[0] + (size_t)K * D
+                                : P.tables[(int)(K >> P.rbits)] + (size_t)(K & rmask) * D;
+#pragma unroll
+    for (int v = 0; v < NVC; ++v) {
+      const int col = lane + 32 * v;
+      if (col < DU) {
+        float4 w = __ldcg(reinterpret_cast<const float4*>(tp) + col);
+        sgd4(w, P.lr, tot[v]);
+        st_f4(tp + 4 * col, w);
+      }
+    }
   }
 }
 
@@ -476,8 +545,14 @@ BwdFn pick_bwd(const BwdParams& P) {
   return pick_bwd_mode<8>(mode);
 }
 
+BwdFn pick_fold(const BwdParams& P) {
+  const int nvc = (P.D / 4 + 31) / 32;
+  return nvc <= 1 ? bwd_fold_kernel<1> : nvc <= 2 ? bwd_fold_kernel<2>
+       : nvc <= 4 ? bwd_fold_kernel<4> : bwd_fold_kernel<8>;
+}
+
 size_t bwd_smem(const BwdParams& P, int threads) {
-  return (size_t)(threads / 32) * ((size_t)2 * P.C * P.D * 4 + 32 * 4 + 32 * 8);
+  return (size_t)(threads / 32) * (size_t)P.wbytes;
 }
 
 }  // namespace
@@ -519,6 +594,11 @@ cudaError_t plan_backward(const BwdParams& P, int threads, int share, unsigned* 
                                                     threads, sm);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
+  // load pass 2's kernel now: with lazy module loading, its first launch behind a running pass 1
+  // (whose CTAs spin on the peers' rows) could otherwise stall the launches the peers need
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(pick_fold(P)));
+  if (e != cudaSuccess) return e;
   long long g = (long long)sms * occ / (share > 1 ? share : 1);
   if (g < 1) g = 1;
   *grid = (unsigned)g;
@@ -531,8 +611,14 @@ cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size
   BwdFn fn = pick_bwd(P);
   BwdParams Pc = P;
   void* args[] = {&Pc};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(threads), args, smem,
-                          st);
+  cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(threads),
+                                   args, smem, st);
+  if (e != cudaSuccess || P.T == 0 || P.nchunks == 0) return e;
+  // pass 2: one warp per chunk (most exit at once)
+  const long long blocks = (P.nchunks + 7) / 8;
+  const unsigned g2 = (unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16);
+  BwdFn f2 = pick_fold(P);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(f2), dim3(g2), dim3(256), args, 0, st);
 }
 
 }  // namespace emba2a

@@ -156,7 +156,7 @@ cudaError_t launch_validate(const int* indices, const int* offsets, long long nn
 // Sort plan: this rank's lookups as (key = t << rbits | row, payload = bag id t*B + j [, weight])
 // sorted stably by key with an LSD radix sort (8-bit digits, one onesweep pass per digit).
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
 constexpr int kMaxPasses = 4;                          // 32-bit keys
 
@@ -198,15 +198,17 @@ struct BwdParams {
   const float* wts;            // sorted weights (weighted plan) or NULL
   const int* offsets;          // bag lengths for mean pooling
   float* const* tables;        // device array of T fp32 table pointers (updated in place)
-  float* scratch;              // [nchunks][D] partial sums of segments that cross chunks
-  unsigned long long* chunk_flag;  // [nchunks] = stamp when scratch[c] is published
+  float* scratch;              // [nchunks][2][D] partial sums of runs crossing chunk edges
+  unsigned char* info;         // [nchunks] bit 0: owns a crossing run, bit 1: inside one
   int* err;
   long long n;                 // lookups in the plan
   long long B, timeout_ns;
   unsigned long long bepoch;   // 1-based fused-backward number (exchange counters, parity)
-  unsigned long long stamp;    // 1-based reduce-launch number (chunk flags)
   float lr;
-  int W, r, T, D, G, toff, C, nchunks, rbits, fused, mean, parity;
+  long long nchunks;           // chunks of kBwdChunk sorted lookups
+  long long wbytes;            // shared memory per warp (finish queue)
+  int flist;                   // finish-queue entries per warp
+  int W, r, T, D, G, toff, rbits, fused, mean, parity;
   long long part[kMaxW + 1];
   int allT[kMaxW];
   int tofs[kMaxW];
@@ -218,10 +220,12 @@ cudaError_t plan_backward(const BwdParams& P, int threads, int share, unsigned* 
                           size_t* smem);
 cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size_t smem,
                             cudaStream_t st);
-// chunk size (lookups per warp work unit) for dimension D
-inline int bwd_chunk(int D) {
+// finish-queue entries per warp for dimension D (<= 8 KB of pooled rows); sorted lookups per
+// warp work unit
+inline int bwd_flist(int D) {
   int c = 2048 / D;
-  return c > 32 ? 32 : (c < 1 ? 1 : c);
+  return c > 16 ? 16 : (c < 2 ? 2 : c);
 }
+constexpr int kBwdChunk = 32;
 
 }  // namespace emba2a

@@ -126,7 +126,6 @@ struct emb_a2a {
   // backward (f3)
   int64_t bwd_threads = 128, bwd_share = 1;
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
-  uint64_t rstamp = 0;                   // reduce launches (chunk-flag stamps)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
   unsigned long long* bflags = nullptr;  // own backward arrival counters
   float* gstage[2] = {nullptr, nullptr}; // own gradient staging [B][T][D] by parity
@@ -138,7 +137,7 @@ struct emb_a2a {
   unsigned long long* d_status = nullptr;
   size_t status_cap = 0;
   float* d_scratch = nullptr;
-  unsigned long long* d_cflag = nullptr;
+  unsigned char* d_info = nullptr;       // per-chunk crossing-run flags (backward pass 2)
   size_t chunk_cap = 0;
   bool planned = false, plan_weighted = false;
   int64_t plan_n = 0;
@@ -220,11 +219,11 @@ void release_registration(emb_a2a* h) {
   if (h->d_hist) cudaFree(h->d_hist);
   if (h->d_status) cudaFree(h->d_status);
   if (h->d_scratch) cudaFree(h->d_scratch);
-  if (h->d_cflag) cudaFree(h->d_cflag);
+  if (h->d_info) cudaFree(h->d_info);
   h->d_hist = nullptr;
   h->d_status = nullptr;
   h->d_scratch = nullptr;
-  h->d_cflag = nullptr;
+  h->d_info = nullptr;
   h->status_cap = h->chunk_cap = 0;
   h->planned = false;
   h->bwd_mode = -1;
@@ -832,7 +831,7 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.offsets = h->plan_offsets;
   P.tables = (float* const*)h->d_tables;
   P.scratch = h->d_scratch;
-  P.chunk_flag = h->d_cflag;
+  P.info = h->d_info;
   P.err = h->d_err;
   P.n = h->planned ? h->plan_n : 0;
   P.B = h->B;
@@ -844,8 +843,9 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.D = h->D;
   P.G = h->G;
   P.toff = h->toff;
-  P.C = bwd_chunk(h->D);
-  P.nchunks = (int)((P.n + P.C - 1) / P.C);
+  P.nchunks = (P.n + kBwdChunk - 1) / kBwdChunk;
+  P.flist = 0;
+  P.wbytes = 32 * (8 + 8 + 4);   // per warp: gradient-row and table-row pointers, scalars
   P.rbits = h->rbits;
   P.fused = fused;
   P.mean = h->mean;
@@ -867,14 +867,12 @@ int run_backward(emb_a2a* h, BwdParams& P, cudaStream_t st) {
     if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "backward plan: %s", cudaGetErrorString(e));
     h->bwd_mode = mode;
   }
-  h->rstamp += 1;
-  P.stamp = h->rstamp;
   cudaError_t e = launch_backward(P, h->bwd_grid, (int)h->bwd_threads, h->bwd_smem, st);
   if (e != cudaSuccess) {
     h->poisoned = true;
     return fail(h, EMB_A2A_ECUDA, "backward kernel launch: %s", cudaGetErrorString(e));
   }
-  h->kernel_launches++;
+  h->kernel_launches += (P.T > 0 && P.nchunks > 0) ? 2 : 1;
   return EMB_A2A_OK;
 }
 
@@ -916,35 +914,36 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   }
   const int64_t n = (h->T > 0) ? num_indices : 0;
   const int passes = (tbits + rbits + 7) / 8;
-  const int C = bwd_chunk(h->D);
-  const int64_t nchunks = (n + C - 1) / C;
+  const int64_t nchunks = (n + kBwdChunk - 1) / kBwdChunk;
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
   // plan storage (grow-only)
+  const size_t ncap = (size_t)n + n / 4 + 4096;   // headroom: batches vary in size
   if ((size_t)n > h->plan_cap) {
     for (int x = 0; x < 2; ++x) {
-      if ((rc = grow(h, &h->d_keys[x], n))) return rc;
-      if ((rc = grow(h, &h->d_bags[x], n))) return rc;
+      if ((rc = grow(h, &h->d_keys[x], ncap))) return rc;
+      if ((rc = grow(h, &h->d_bags[x], ncap))) return rc;
     }
-    h->plan_cap = n;
+    h->plan_cap = ncap;
   }
   if (wtd && (size_t)n > h->wts_cap) {
     for (int x = 0; x < 2; ++x)
-      if ((rc = grow(h, &h->d_wts[x], n))) return rc;
-    h->wts_cap = n;
+      if ((rc = grow(h, &h->d_wts[x], ncap))) return rc;
+    h->wts_cap = ncap;
   }
   if (!h->d_hist && (rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses))) return rc;
   const size_t nstatus = (size_t)passes * ntiles * 256;
   if (nstatus > h->status_cap) {
-    if ((rc = grow(h, &h->d_status, nstatus))) return rc;
-    CUDA_TRY(h, cudaMemset(h->d_status, 0, nstatus * 8));
-    h->status_cap = nstatus;
+    const size_t scap = nstatus + nstatus / 4 + 4 * 256;
+    if ((rc = grow(h, &h->d_status, scap))) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->d_status, 0, scap * 8, st));   // ordered before the plan
+    h->status_cap = scap;
   }
   if ((size_t)nchunks > h->chunk_cap) {
-    if ((rc = grow(h, &h->d_scratch, (size_t)nchunks * h->D))) return rc;
-    if ((rc = grow(h, &h->d_cflag, nchunks))) return rc;
-    CUDA_TRY(h, cudaMemset(h->d_cflag, 0, (size_t)nchunks * 8));
-    h->chunk_cap = nchunks;
+    const size_t cap = (size_t)nchunks + nchunks / 4 + 64;    // headroom: batches vary in size
+    if ((rc = grow(h, &h->d_scratch, cap * 2 * h->D))) return rc;
+    if ((rc = grow(h, &h->d_info, cap))) return rc;
+    h->chunk_cap = cap;
   }
   h->plan_no += 1;
   h->rbits = rbits;
@@ -989,7 +988,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long TB = (long long)h->T * h->B;
-  const long long gk = std::min<long long>((TB + 255) / 256, (long long)sms * 8);
+  const long long gk = std::min<long long>((TB + 63) / 64, (long long)sms * 8);   // 8 bags/warp
   cudaError_t e = launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1), st);
   if (e != cudaSuccess) {
     h->planned = false;
@@ -1028,6 +1027,11 @@ int emb_a2a_backward_local(emb_a2a_t* h, const float* grad_mp, float lr, void* s
   DeviceGuard guard(h->dev);
   BwdParams P = bwd_params(h, grad_mp, lr, 0);
   return run_backward(h, P, (cudaStream_t)stream);
+}
+
+int emb_a2a_check(emb_a2a_t* h) {
+  if (!h) return EMB_A2A_EINVAL;
+  return check_async(h);
 }
 
 int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
@@ -1111,6 +1115,7 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (v > 0) {
       CUDA_TRY(h, cudaMalloc((void**)&h->d_trace, (size_t)(2 + 2 * v) * 8));
       CUDA_TRY(h, cudaMemset(h->d_trace, 0, (size_t)(2 + 2 * v) * 8));
+      CUDA_TRY(h, cudaDeviceSynchronize());   // legacy-stream memset vs. non-blocking streams
       h->trace_cap = v;
     }
   } else if (k == "bwd_threads") {
@@ -1182,7 +1187,7 @@ int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "backward_epoch") *v = (int64_t)h->bepoch;
   else if (k == "plan_lookups") *v = h->planned ? h->plan_n : -1;
   else if (k == "bwd_grid") *v = h->bwd_grid;
-  else if (k == "bwd_chunk") *v = bwd_chunk(h->D);
+  else if (k == "bwd_chunk") *v = kBwdChunk;
   else if (k.rfind("expected_in:", 0) == 0) {
     const int q = atoi(k.c_str() + 12);
     if (q < 0 || q >= h->W) return EMB_A2A_EINVAL;
@@ -1225,6 +1230,7 @@ int emb_a2a_read_trace(emb_a2a_t* h, uint64_t* out, int64_t capacity, int64_t* n
   if (capacity < m || (!out && m > 0)) return fail(h, EMB_A2A_EINVAL, "capacity < %lld", (long long)m);
   if (m > 0) CUDA_TRY(h, cudaMemcpy(out, h->d_trace + 2, (size_t)m * 16, cudaMemcpyDeviceToHost));
   CUDA_TRY(h, cudaMemset(h->d_trace, 0, 8));   // restart the log
+  CUDA_TRY(h, cudaDeviceSynchronize());
   return EMB_A2A_OK;
 }
 

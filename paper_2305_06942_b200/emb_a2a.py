@@ -255,6 +255,10 @@ class EmbA2A:
                                         float(lr), _stream_ptr(stream, self.device))
         self._err(rc, "emb_a2a_backward_local")
 
+    def check(self) -> None:
+        """Raise if an asynchronous device failure (a wait timeout) was recorded."""
+        self._err(lib.emb_a2a_check(self._h), "emb_a2a_check")
+
     def device_barrier(self, stream=None) -> None:
         """Collective: the stream waits on the device until every rank has arrived."""
         self._err(lib.emb_a2a_device_barrier(self._h, _stream_ptr(stream, self.device)),

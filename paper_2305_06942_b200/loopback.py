@@ -64,23 +64,35 @@ class LoopbackGroup:
                  grads: Sequence[torch.Tensor], lr: float, sync: bool = True,
                  weights: Optional[Sequence[torch.Tensor]] = None, plan: bool = True) -> None:
         """Plan (sort) + fused backward on every virtual rank, W streams.  The backward's
-        persistent grid is shared W ways so all W kernels are resident together (each waits for
-        the others' gradient rows)."""
+        persistent grid is shared W+1 ways so all W kernels are resident together with room to
+        spare (each waits for the others' gradient rows)."""
         cur = torch.cuda.current_stream(self.device)
+        share = self.W + 1 if self.W > 1 else 1   # slack: the grids must co-reside exactly
         for r, h in enumerate(self.handles):
-            if h.get_option("bwd_share") != self.W:
-                h.set_option("bwd_share", self.W)
+            if h.get_option("bwd_share") != share:
+                h.set_option("bwd_share", share)
             self.streams[r].wait_stream(cur)
         if plan:
             for r, h in enumerate(self.handles):
                 h.backward_plan(indices[r], offsets[r], stream=self.streams[r],
                                 per_sample_weights=None if weights is None else weights[r])
+            # every plan before any backward: on ONE device the W persistent backward grids fill
+            # the GPU while they wait for each other's gradient rows, so a plan still queued
+            # behind them could never get an SM (on W GPUs each plan has its own device)
+            done = [torch.cuda.Event() for _ in range(self.W)]
+            for r in range(self.W):
+                done[r].record(self.streams[r])
+            for r in range(self.W):
+                for e in done:
+                    self.streams[r].wait_event(e)
         for r, h in enumerate(self.handles):
             h.backward(grads[r], lr, stream=self.streams[r])
         for s in self.streams:
             cur.wait_stream(s)
         if sync:
             torch.cuda.synchronize(self.device)
+            for h in self.handles:
+                h.check()
 
     def destroy(self):
         run_ranks(lambda r: self.handles[r].destroy(), self.W)

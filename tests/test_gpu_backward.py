@@ -151,8 +151,9 @@ def test_backward_variants(mode):
     bound_check(p, got, want, grads, 0.1, weights=weights, pooling=pooling)
 
 
+@pytest.mark.parametrize("threads", [128, 32])
 @pytest.mark.parametrize("D", [4, 64, 256, 1024])
-def test_hot_row_spanning_many_chunks(D):
+def test_hot_row_spanning_many_chunks(D, threads):
     """One row looked up thousands of times (a Zipf head): its run crosses hundreds of chunks
     and more than one 32-chunk look-back window; exact-int grads -> bitwise."""
     B, W = 256, 2
@@ -165,8 +166,49 @@ def test_hot_row_spanning_many_chunks(D):
     p = Problem(W, [1, 1], D, B, synth.even_partition(B, W), [tab, tab2], [i, i2], [o, o2])
     grads = grads_for(p, 1, 1)
     want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 1.0)
-    run = Run(p)
+    run = Run(p, opts={"bwd_threads": threads})
     run.backward(grads, 1.0)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+@pytest.mark.parametrize("shift", [0, 1, 17, 31])
+def test_runs_around_chunk_edges(shift):
+    """Runs of length C-1, C, C+1, 2C+3, 33C (C = 32 lookups per chunk) shifted so that they
+    start and end at every offset of a chunk: runs inside a chunk are finished there, runs that
+    cross chunk edges are folded from per-chunk partials (pass 2).  Exact-int -> bitwise."""
+    D, B = 8, 64
+    unit = 32
+    lens = [shift + 1, unit - 1, 3, unit, unit + 1, 2, 2 * unit + 3, 5, unit - 1, unit + 1, 7,
+            33 * unit, 1, 1, 64 * unit + 5]
+    rows = []
+    for x, L in enumerate(lens):
+        rows += [x] * L
+    # spread the lookups over the bags in order (one table), several per bag
+    per = (len(rows) + B - 1) // B
+    bags = [rows[j * per:(j + 1) * per] for j in range(B)]
+    i, o = csr_from_bags([bags])
+    rng = np.random.default_rng(unit)
+    tab = rng.integers(-8, 8, (len(lens), D)).astype(np.float32)
+    p = Problem(1, [1], D, B, np.array([0, B]), [tab], [i], [o])
+    grads = grads_for(p, 2, 1)
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, -1.0)
+    run = Run(p)
+    run.backward(grads, -1.0)
+    np.testing.assert_array_equal(run.tables()[0], want[0])
+    assert run.g.handles[0].query("bwd_chunk") == unit
+    run.destroy()
+
+
+@pytest.mark.parametrize("threads", [128, 64])
+@pytest.mark.parametrize("seed", range(4))
+def test_random_exact_any_grid(seed, threads):
+    p = random_problem(5600 + seed, value_mode=1, ragged=True, max_B=128, max_D=64)
+    grads = grads_for(p, seed, 1)
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 2.0)
+    run = Run(p, opts={"bwd_threads": threads})
+    run.backward(grads, 2.0)
     for a, b in zip(run.tables(), want):
         np.testing.assert_array_equal(a, b)
     run.destroy()
