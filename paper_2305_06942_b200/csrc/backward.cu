@@ -43,6 +43,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -177,21 +182,32 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     st_relaxed_gpu(my, lb_word(P.stamp, 2, run));
   } else {
     st_relaxed_gpu(my, lb_word(P.stamp, 1, run));
+    // look back 8 tiles per round trip: read the window's words together, then take them in
+    // order from the nearest, stopping at the first inclusive prefix; a word not yet published
+    // is re-read alone (tiles are taken in ticket order, so every predecessor is running and
+    // will publish; the time bound only guards against a broken invariant hanging the GPU)
     long long look = tile - 1;
     const unsigned want = P.stamp & 0x3fffffffu;
     const unsigned long long t0 = globaltimer();
-    while (look >= 0) {
-      const unsigned long long v = ld_acquire_gpu(P.status + look * 256 + d);
-      const unsigned flag = (unsigned)(v >> 32) & 3u;
-      if ((unsigned)(v >> 34) != want || flag == 0u) {   // predecessor not published yet
-        // tiles are taken in ticket order, so every predecessor is running and will publish;
-        // the bound only guards against a broken invariant turning into a hung GPU
-        if (globaltimer() - t0 > 5000000000ull) break;
-        continue;
+    bool done = false;
+    while (look >= 0 && !done) {
+      constexpr int LB = 8;
+      unsigned long long v[LB];
+#pragma unroll
+      for (int i = 0; i < LB; ++i)
+        v[i] = (look - i >= 0) ? ld_relaxed_gpu(P.status + (look - i) * 256 + d) : 0ull;
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        if (done || look - i < 0) continue;
+        unsigned long long w = v[i];
+        while ((unsigned)(w >> 34) != want || ((unsigned)(w >> 32) & 3u) == 0u) {
+          if (globaltimer() - t0 > 5000000000ull) break;
+          w = ld_relaxed_gpu(P.status + (look - i) * 256 + d);
+        }
+        excl += (unsigned)w;
+        if (((unsigned)(w >> 32) & 3u) == 2u) done = true;
       }
-      excl += (unsigned)v;
-      if (flag == 2u) break;
-      --look;
+      look -= LB;
     }
     st_relaxed_gpu(my, lb_word(P.stamp, 2, excl + run));
   }
@@ -228,6 +244,8 @@ template <int NVC, int MODE>
 __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : 4) bwd_kernel(const __grid_constant__ BwdParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_pushed[kMaxW];
+  __shared__ float* s_tab[kMaxSmemTables];   // this rank's table pointers (T <= 256)
+  __shared__ long long s_ticket[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int D = P.D, DU = D >> 2;
 
@@ -292,171 +310,256 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : 4) bwd_kernel(const __grid
     __syncthreads();
   }
   if (P.T == 0 || P.n == 0) return;
+  for (int t = tid; t < P.T && t < kMaxSmemTables; t += blockDim.x) s_tab[t] = P.tables[t];
+  __syncthreads();
+  float* const* tabs = P.T <= kMaxSmemTables ? s_tab : P.tables;
 
-  // ---- reduce + update, pass 1 (R#31).  Work unit = a chunk of 32 consecutive sorted lookups
-  // per warp.  The chunk's runs (pieces of equal keys) are split into NG contiguous ranges, one
-  // per lane group (LPG lanes cover a row); a group walks its range in sorted order with UF
-  // gradient rows in flight per lane and sums each run in ascending lookup order -- the
-  // row-flattened pooling loop of the forward, with runs for bags.  A run that starts and ends
-  // inside the chunk is finished here: queued (row, sum) in the group's registers and applied
-  // in batches (all table-row loads in flight together).  The chunk's first run, if it began in
-  // an earlier chunk, and its last run, if it goes on into the next, are left as partial sums
-  // in the chunk's two scratch slots for pass 2 (bwd_fold_kernel).
-  constexpr int UF = NVC >= 8 ? 1 : 8 / NVC;
-  constexpr int QN = NVC >= 4 ? 2 : 4;                 // finished-run queue per group
+  // ---- reduce + update, pass 1 (R#31).  Work unit = a chunk of kBwdChunk consecutive sorted
+  // lookups per warp, taken 32 at a time (sub-batches).  A sub-batch's runs (pieces of equal
+  // keys) are split into NG contiguous ranges, one per lane group (LPG lanes cover a row); a
+  // group walks its range in sorted order with UF gradient rows in flight per lane and sums each
+  // run in ascending lookup order -- the row-flattened pooling loop of the forward, with runs for
+  // bags.  A run going on into the next sub-batch hands its sum over through shared memory.  A
+  // run that starts and ends inside the chunk is finished here: queued (row, sum) in the group's
+  // registers and applied in batches (all table-row loads in flight together).  The chunk's
+  // first run, if it began in an earlier chunk, and its last run, if it goes on into the next
+  // chunk, are left as partial sums in the chunk's two scratch slots for pass 2.
+  constexpr int UF = NVC >= 8 ? 1 : 8 / NVC;          // lookups in flight per lane
   int LPG = 1;
   while (LPG < DU && LPG < 32) LPG <<= 1;
   const int NG = 32 / LPG, grp = lane / LPG, gl = lane - grp * LPG;
-  const long long* sptr = reinterpret_cast<const long long*>(smem + (size_t)warp * P.wbytes);
-  long long* wsrc = reinterpret_cast<long long*>(smem + (size_t)warp * P.wbytes);   // [32] rows
-  long long* wtab = wsrc + 32;                                                      // [32] table
-  float* wsc = reinterpret_cast<float*>(wtab + 32);                                 // [32] scale
-  (void)sptr;
+  long long* wsrc = reinterpret_cast<long long*>(smem + (size_t)warp * P.wbytes);  // [32] rows
+  long long* wtab = wsrc + 32;                                                     // [32] table
+  float* wsc = reinterpret_cast<float*>(wtab + 32);                                // [32] scale
+  float* carry0 = wsc + 32;                                           // [2][D] carried sums
   const unsigned rmask = P.rbits >= 32 ? 0xffffffffu : ((1u << P.rbits) - 1u);
   const long long gw = (long long)blockIdx.x * nw + warp, nwt = (long long)gridDim.x * nw;
   const long long pr = P.part[P.r];
   const long long n = P.n;
+  const unsigned B32 = (unsigned)P.B;
   const unsigned* __restrict__ keys = P.keys;
-  float4 qacc[QN][NVC];
-  float* qtab[QN];
-  int nq = 0;
 
-  auto flush = [&]() {                               // this group's queued rows: SGD step
-    float4 w[QN][NVC];
-#pragma unroll
-    for (int f = 0; f < QN; ++f)
-#pragma unroll
-      for (int v = 0; v < NVC; ++v) {
-        const int col = gl + LPG * v;
-        w[f][v] = (f < nq && col < DU) ? __ldcg(reinterpret_cast<const float4*>(qtab[f]) + col)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-    for (int f = 0; f < QN; ++f)
-      if (f < nq)
-#pragma unroll
-        for (int v = 0; v < NVC; ++v) {
-          const int col = gl + LPG * v;
-          if (col < DU) {
-            sgd4(w[f][v], P.lr, qacc[f][v]);
-            st_f4(qtab[f] + 4 * col, w[f][v]);
-          }
-        }
-    nq = 0;
-  };
-
-  for (long long c = gw; c < P.nchunks; c += nwt) {
+  (void)gw;
+  (void)nwt;
+  while (true) {
+    // chunks handed out by ticket (P.ticket zeroed before the launch): a warp that drew
+    // cheap chunks takes more
+    if (lane == 0) s_ticket[warp] = (long long)atomicAdd(P.ticket, 1u);
+    __syncwarp();
+    const long long c = s_ticket[warp];
+    __syncwarp();
+    if (c >= P.nchunks) break;
     const long long p0 = c * kBwdChunk;
-    const int len = (n - p0) < kBwdChunk ? (int)(n - p0) : kBwdChunk;
-    unsigned key = 0u;
-    int bag = 0;
-    if (lane < len) {
+    const int clen = (n - p0) < kBwdChunk ? (int)(n - p0) : kBwdChunk;
+    // sub-batch 0's lookups; the keys just before and just after the chunk
+    unsigned key = 0u, nkey = 0u;
+    int bag = 0, nbag = 0;
+    if (lane < clen) {
       key = keys[p0 + lane];
       bag = P.bags[p0 + lane];
     }
-    const unsigned kup = __shfl_up_sync(kFull, key, 1);
-    const unsigned startm = __ballot_sync(kFull, lane < len && (lane == 0 || key != kup));
-    const unsigned key0 = __shfl_sync(kFull, key, 0);
-    const unsigned keyl = __shfl_sync(kFull, key, len - 1);
-    int flags = 0;
+    int cf = 0;
     if (lane == 0) {
-      if (p0 > 0 && keys[p0 - 1] == key0) flags |= 1;              // first run continues in
-      if (p0 + len < n && keys[p0 + len] == keyl) flags |= 2;       // last run continues out
+      if (p0 > 0 && keys[p0 - 1] == key) cf |= 1;                         // run enters chunk
+      if (p0 + clen < n && keys[p0 + clen] == keys[p0 + clen - 1]) cf |= 2;   // run leaves
     }
-    flags = __shfl_sync(kFull, flags, 0);
-    const bool cont_in = flags & 1, cont_out = flags & 2;
-    const int npieces = __popc(startm);
-    // per lookup: where its gradient row lives, its scalar, the row it updates
-    __syncwarp();                                    // previous chunk's readers are done
-    if (lane < len) {
-      const int t = (int)(bag / P.B);
-      const long long j = bag - (long long)t * P.B;
-      int s = 0;
-      while (P.part[s + 1] <= j) ++s;                  // destination of bag j
-      const float* src;
-      if (P.fused)
-        src = (s == P.r) ? P.grad + ((j - pr) * P.G + P.toff + t) * D
-                         : P.stage + (j * P.T + t) * D;
-      else
-        src = P.grad + (j * P.T + t) * D;
-      wsrc[lane] = reinterpret_cast<long long>(src);
-      wtab[lane] = reinterpret_cast<long long>(
-          (P.rbits >= 32) ? P.tables[0] + (size_t)key * D
-                          : P.tables[(int)(key >> P.rbits)] + (size_t)(key & rmask) * D);
-      if (MODE == 1) wsc[lane] = P.wts[p0 + lane];
-      if (MODE == 2) wsc[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
-      if (lane == 0) {
-        const bool inside = npieces == 1 && cont_in && cont_out;    // one run covers the chunk
-        P.info[c] = (unsigned char)((cont_out && !inside ? 1 : 0) | (inside ? 2 : 0));
+    cf = __shfl_sync(kFull, cf, 0);
+    const bool chunk_in = cf & 1, chunk_out = cf & 2;
+    bool ob = chunk_in;          // the run entering the current sub-batch began before the chunk
+    unsigned prev_last = 0u;     // last key of the previous sub-batch
+    const int nsb = (clen + 31) / 32;
+    for (int sb = 0; sb < nsb; ++sb) {
+      const long long pb = p0 + 32 * sb;
+      const int len = (clen - 32 * sb) < 32 ? clen - 32 * sb : 32;
+      const bool last_sb = sb == nsb - 1;
+      if (!last_sb) {                                // prefetch the next sub-batch
+        const int nl = (clen - 32 * (sb + 1)) < 32 ? clen - 32 * (sb + 1) : 32;
+        if (lane < nl) {
+          nkey = keys[pb + 32 + lane];
+          nbag = P.bags[pb + 32 + lane];
+        }
       }
-    }
-    __syncwarp();
-    // this group's runs [pa, pb) = positions [lo, hi)
-    const int pa = (npieces * grp) / NG, pb = (npieces * (grp + 1)) / NG;
-    if (pa < pb) {
-      const int lo = __fns(startm, 0, pa + 1);
-      const int hi = pb < npieces ? (int)__fns(startm, 0, pb + 1) : len;
-      int pi = pa;
-      float4 acc[NVC];
-#pragma unroll
-      for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q0 = lo; q0 < hi; q0 += UF) {
-        float4 buf[UF][NVC];
-#pragma unroll
-        for (int x = 0; x < UF; ++x) {
-          const int q = q0 + x;
-          const float4* rp = reinterpret_cast<const float4*>(wsrc[q < hi ? q : lo]);
+      const unsigned kup = __shfl_up_sync(kFull, key, 1);
+      const unsigned startm = __ballot_sync(kFull, lane < len && (lane == 0 || key != kup));
+      const unsigned key0 = __shfl_sync(kFull, key, 0);
+      const unsigned keyl = __shfl_sync(kFull, key, len - 1);
+      const bool in_sb = sb == 0 ? chunk_in : (key0 == prev_last);
+      const bool out_sb = last_sb ? chunk_out : (__shfl_sync(kFull, nkey, 0) == keyl);
+      const int npieces = __popc(startm);
+      __syncwarp();                                  // the previous sub-batch's readers are done
+      if (lane < len) {
+        const unsigned t = (unsigned)bag / B32;
+        const long long j = (long long)((unsigned)bag - t * B32);
+        int s = 0;
+        while (P.part[s + 1] <= j) ++s;              // destination of bag j
+        const float* src;
+        if (P.fused)
+          src = (s == P.r) ? P.grad + ((j - pr) * P.G + P.toff + (int)t) * D
+                           : P.stage + (j * P.T + (int)t) * D;
+        else
+          src = P.grad + (j * P.T + (int)t) * D;
+        wsrc[lane] = reinterpret_cast<long long>(src);
+        wtab[lane] = reinterpret_cast<long long>(
+            (P.rbits >= 32) ? tabs[0] + (size_t)key * D
+                            : tabs[(int)(key >> P.rbits)] + (size_t)(key & rmask) * D);
+        if (MODE == 1) wsc[lane] = P.wts[pb + lane];
+        if (MODE == 2) wsc[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
+      }
+      if (sb == 0 && lane == 0) {
+        const bool inside = chunk_in && chunk_out && npieces == 1 && nsb == 1;
+        // pass-2 flags, fixed up below once we know whether the last run began before the chunk
+        P.info[c] = (unsigned char)((chunk_out && !inside ? 1 : 0) | (inside ? 2 : 0));
+      }
+      __syncwarp();
+      bool carry_out = false, carry_ob = false;
+      const float* cin = carry0 + (size_t)(sb & 1) * D;      // written in sub-batch sb - 1
+      float* cout = carry0 + (size_t)((sb + 1) & 1) * D;
+
+      // Finish the piece (run, or part of one) ending at lookup q with sum acc.
+      auto finish = [&](float4 (&acc)[NVC], int q, int pi, bool enters, bool has_w,
+                        const float4 (&cur_w)[NVC]) {
+        const bool leaves = pi == npieces - 1 && out_sb;
+        const bool began_before = enters && ob;      // the run began in an earlier chunk
+        if (leaves && !last_sb) {                    // hand over to the next sub-batch
+          carry_out = true;
+          carry_ob = began_before;
 #pragma unroll
           for (int v = 0; v < NVC; ++v) {
             const int col = gl + LPG * v;
-            buf[x][v] = (q < hi && col < DU) ? __ldcg(rp + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (col < DU) st_shared_f4(cout + 4 * col, acc[v]);
           }
-        }
-#pragma unroll
-        for (int x = 0; x < UF; ++x) {
-          const int q = q0 + x;
-          if (q >= hi) break;
-          const float s = (MODE != 0) ? wsc[q] : 1.f;
+        } else if (leaves || began_before) {         // partial for pass 2
+          float* slot = P.scratch + ((size_t)c * 2 + (leaves ? 1 : 0)) * D;
 #pragma unroll
           for (int v = 0; v < NVC; ++v) {
-            float4 cv = buf[x][v];
-            if (MODE == 1) {
-              cv.x = __fmul_rn(s, cv.x); cv.y = __fmul_rn(s, cv.y);
-              cv.z = __fmul_rn(s, cv.z); cv.w = __fmul_rn(s, cv.w);
-            } else if (MODE == 2) {
-              cv.x = __fdiv_rn(cv.x, s); cv.y = __fdiv_rn(cv.y, s);
-              cv.z = __fdiv_rn(cv.z, s); cv.w = __fdiv_rn(cv.w, s);
-            }
-            add4(acc[v], cv);
+            const int col = gl + LPG * v;
+            if (col < DU) st_f4(slot + 4 * col, acc[v]);
           }
-          if (q + 1 < len && !((startm >> (q + 1)) & 1u)) continue;   // run goes on
-          // ---- the run ending at lookup q: finished here, or a partial for pass 2
-          const bool part_in = pi == 0 && cont_in, part_out = pi == npieces - 1 && cont_out;
-          if (part_in || part_out) {
-            float* slot = P.scratch + ((size_t)c * 2 + (part_out ? 1 : 0)) * D;
+          if (leaves && gl == 0)                     // owner iff the run began in this chunk
+            P.info[c] = (unsigned char)(began_before ? 2 : 1);
+        } else {                                     // finished here: the SGD step
+          float* tp = reinterpret_cast<float*>(wtab[q]);
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            const int col = gl + LPG * v;
+            if (col < DU) {
+              // a run handed over from the previous sub-batch loads its row now
+              float4 w = has_w ? cur_w[v] : __ldcg(reinterpret_cast<const float4*>(tp) + col);
+              sgd4(w, P.lr, acc[v]);
+              st_f4(tp + 4 * col, w);
+            }
+          }
+        }
+      };
+
+      // Sum lookups [lo, hi) in order into acc (UF rows in flight per lane); at each run end
+      // inside the range call finish (split = false), else just accumulate (split = true).
+      // The table row of a run starting in the range is loaded with its first gradient row.
+      auto walk = [&](float4 (&acc)[NVC], int lo, int hi, int pi, bool enters, bool split,
+                      bool& has_w, float4 (&cur_w)[NVC]) {
+        for (int q0 = lo; q0 < hi; q0 += UF) {
+          float4 buf[UF][NVC], tw[UF][NVC];
+#pragma unroll
+          for (int x = 0; x < UF; ++x) {
+            const int q = q0 + x;
+            const bool ok = q < hi;
+            const bool st = ok && ((startm >> q) & 1u) && !(q == 0 && in_sb);
+            const float4* rp = reinterpret_cast<const float4*>(wsrc[ok ? q : lo]);
+            const float4* tp = reinterpret_cast<const float4*>(wtab[ok ? q : lo]);
 #pragma unroll
             for (int v = 0; v < NVC; ++v) {
               const int col = gl + LPG * v;
-              if (col < DU) st_f4(slot + 4 * col, acc[v]);
+              buf[x][v] = (ok && col < DU) ? __ldcg(rp + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+              tw[x][v] = (st && col < DU) ? __ldcg(tp + col) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-          } else {
-#pragma unroll
-            for (int f = 0; f < QN; ++f)
-              if (f == nq) {
-#pragma unroll
-                for (int v = 0; v < NVC; ++v) qacc[f][v] = acc[v];
-                qtab[f] = reinterpret_cast<float*>(wtab[q]);
-              }
-            if (++nq == QN) flush();
           }
 #pragma unroll
-          for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-          ++pi;
+          for (int x = 0; x < UF; ++x) {
+            const int q = q0 + x;
+            if (q >= hi) break;
+            if (((startm >> q) & 1u) && !(q == 0 && in_sb)) {
+#pragma unroll
+              for (int v = 0; v < NVC; ++v) cur_w[v] = tw[x][v];
+              has_w = true;
+            }
+            const float s = (MODE != 0) ? wsc[q] : 1.f;
+#pragma unroll
+            for (int v = 0; v < NVC; ++v) {
+              float4 cv = buf[x][v];
+              if (MODE == 1) {
+                cv.x = __fmul_rn(s, cv.x); cv.y = __fmul_rn(s, cv.y);
+                cv.z = __fmul_rn(s, cv.z); cv.w = __fmul_rn(s, cv.w);
+              } else if (MODE == 2) {
+                cv.x = __fdiv_rn(cv.x, s); cv.y = __fdiv_rn(cv.y, s);
+                cv.z = __fdiv_rn(cv.z, s); cv.w = __fdiv_rn(cv.w, s);
+              }
+              add4(acc[v], cv);
+            }
+            if (split || (q + 1 < len && !((startm >> (q + 1)) & 1u))) continue;
+            finish(acc, q, pi, enters, has_w, cur_w);
+#pragma unroll
+            for (int v = 0; v < NVC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ++pi;
+            enters = false;
+            has_w = false;
+          }
+        }
+      };
+
+      float4 acc[NVC], cur_w[NVC];
+      bool has_w = false;
+#pragma unroll
+      for (int v = 0; v < NVC; ++v) {
+        acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        cur_w[v] = acc[v];
+      }
+      if (npieces == 1 && NG > 1) {
+        // one run fills the sub-batch (a Zipf-hot row): every lane group sums an equal share of
+        // its lookups, then the shares are added in group order (after the carried-in sum)
+        walk(acc, (len * grp) / NG, (len * (grp + 1)) / NG, 0, false, true, has_w, cur_w);
+        const bool enters = in_sb;
+        float4 tot[NVC];
+#pragma unroll
+        for (int v = 0; v < NVC; ++v) {
+          const int col = gl + LPG * v;
+          tot[v] = (enters && sb > 0 && col < DU) ? lds_f4(smem_u32(cin + 4 * col))
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int g = 0; g < NG; ++g) {
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            float4 p;
+            p.x = __shfl_sync(kFull, acc[v].x, g * LPG + gl);
+            p.y = __shfl_sync(kFull, acc[v].y, g * LPG + gl);
+            p.z = __shfl_sync(kFull, acc[v].z, g * LPG + gl);
+            p.w = __shfl_sync(kFull, acc[v].w, g * LPG + gl);
+            add4(tot[v], p);
+          }
+        }
+        if (grp == 0) finish(tot, len - 1, 0, enters, has_w, cur_w);
+      } else {
+        const int pa = (npieces * grp) / NG, pbnd = (npieces * (grp + 1)) / NG;
+        if (pa < pbnd) {
+          const int lo = __fns(startm, 0, pa + 1);
+          const int hi = pbnd < npieces ? (int)__fns(startm, 0, pbnd + 1) : len;
+          const bool enters = pa == 0 && in_sb;
+#pragma unroll
+          for (int v = 0; v < NVC; ++v) {
+            const int col = gl + LPG * v;
+            if (enters && sb > 0 && col < DU) acc[v] = lds_f4(smem_u32(cin + 4 * col));
+          }
+          walk(acc, lo, hi, pa, enters, false, has_w, cur_w);
         }
       }
+      // which group (if any) carried a run over, and whether it began before the chunk
+      const unsigned cm = __ballot_sync(kFull, carry_out);
+      if (cm) ob = __shfl_sync(kFull, carry_ob, __ffs(cm) - 1);
+      else ob = false;
+      prev_last = keyl;
+      key = nkey;
+      bag = nbag;
     }
   }
-  if (nq > 0) flush();
 }
 
 // ---- reduce + update, pass 2 (R#31): the runs that cross chunk boundaries.  The chunk a run

@@ -200,6 +200,7 @@ struct BwdParams {
   float* const* tables;        // device array of T fp32 table pointers (updated in place)
   float* scratch;              // [nchunks][2][D] partial sums of runs crossing chunk edges
   unsigned char* info;         // [nchunks] bit 0: owns a crossing run, bit 1: inside one
+  unsigned* ticket;            // pass-1 chunk tickets (zeroed before each launch)
   int* err;
   long long n;                 // lookups in the plan
   long long B, timeout_ns;
@@ -226,6 +227,6 @@ inline int bwd_flist(int D) {
   int c = 2048 / D;
   return c > 16 ? 16 : (c < 2 ? 2 : c);
 }
-constexpr int kBwdChunk = 32;
+constexpr int kBwdChunk = 64;    // sorted lookups per warp work unit (2 sub-batches of 32)
 
 }  // namespace emba2a

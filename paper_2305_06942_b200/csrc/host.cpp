@@ -832,6 +832,7 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.tables = (float* const*)h->d_tables;
   P.scratch = h->d_scratch;
   P.info = h->d_info;
+  P.ticket = h->d_hist + kMaxPasses * 256 + kMaxPasses;
   P.err = h->d_err;
   P.n = h->planned ? h->plan_n : 0;
   P.B = h->B;
@@ -845,7 +846,8 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.toff = h->toff;
   P.nchunks = (P.n + kBwdChunk - 1) / kBwdChunk;
   P.flist = 0;
-  P.wbytes = 32 * (8 + 8 + 4);   // per warp: gradient-row and table-row pointers, scalars
+  // per warp: gradient-row and table-row pointers and scalars of a sub-batch, a carried sum
+  P.wbytes = 32 * (8 + 8 + 4) + 2 * (int64_t)h->D * 4;
   P.rbits = h->rbits;
   P.fused = fused;
   P.mean = h->mean;
@@ -867,6 +869,8 @@ int run_backward(emb_a2a* h, BwdParams& P, cudaStream_t st) {
     if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "backward plan: %s", cudaGetErrorString(e));
     h->bwd_mode = mode;
   }
+  if (P.T > 0 && P.n > 0)
+    CUDA_TRY(h, cudaMemsetAsync(P.ticket, 0, sizeof(unsigned), st));
   cudaError_t e = launch_backward(P, h->bwd_grid, (int)h->bwd_threads, h->bwd_smem, st);
   if (e != cudaSuccess) {
     h->poisoned = true;
@@ -931,7 +935,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
       if ((rc = grow(h, &h->d_wts[x], ncap))) return rc;
     h->wts_cap = ncap;
   }
-  if (!h->d_hist && (rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses))) return rc;
+  // [pass histograms | pass tile tickets | backward chunk ticket]
+  if (!h->d_hist && (rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses + 1))) return rc;
   const size_t nstatus = (size_t)passes * ntiles * 256;
   if (nstatus > h->status_cap) {
     const size_t scap = nstatus + nstatus / 4 + 4 * 256;
