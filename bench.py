@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--no-baseline", action="store_true", help="skip the unfused NCCL baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-backward", action="store_true", help="skip the f3 backward timing")
+    ap.add_argument("--table-dtype", default="f32", choices=["f32", "bf16", "f16"],
+                    help="table element type (f2; fp32 accumulation and output either way)")
+    ap.add_argument("--pooling", default="sum", choices=["sum", "mean"], help="f2: mean pooling")
+    ap.add_argument("--weighted", action="store_true", help="f2: per-sample weights")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
     return ap.parse_args()
@@ -79,12 +83,14 @@ def workload_desc(cfg):
             f"global batch {cfg.B}, {pool}, Zipf alpha={cfg.alpha}, fp32")
 
 
-def algorithmic_bytes(cfg, r, nnz):
-    """Per-rank algorithmic bytes of one forward: gathered rows + indices +
-    offsets + this rank's receive buffer; and the bytes it must send over NVLink."""
+def algorithmic_bytes(cfg, r, nnz, esize=4, weighted=False):
+    """Per-rank algorithmic bytes of one forward: gathered rows (esize bytes
+    per element) + indices (+ weights) + offsets + this rank's receive buffer; and the bytes it
+    must send over NVLink."""
     b = int(cfg.part[r + 1] - cfg.part[r])
     T = cfg.T[r]
-    hbm = nnz * cfg.D * 4 + nnz * 4 + (T * cfg.B + 1) * 4 + b * cfg.G * cfg.D * 4
+    hbm = nnz * cfg.D * esize + nnz * (8 if weighted else 4) + (T * cfg.B + 1) * 4 + \
+        b * cfg.G * cfg.D * 4
     tx = (cfg.B - b) * T * cfg.D * 4
     return hbm, tx
 
@@ -266,6 +272,13 @@ def main():
         dist.all_reduce(t)
         nnz_all.append(int(t.item()))
     tables = sdev.rank_tables(cfg, rank, dev)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[args.table_dtype]
+    if tdt != torch.float32:      # exact conversion of the procedural fp32 values (R#28)
+        tables = [t.to(tdt) for t in tables]
+    d_w = None
+    if args.weighted:
+        d_w = [torch.from_numpy(synth.gen_weights(cfg, rank, mine[k][0].size, batch=k)).to(dev)
+               for k in range(args.batches)]
     torch.cuda.synchronize()
 
     h = EmbA2A(rank, N, dev, torch_allgather(None, dev), {"timeout_ms": 60000} if shared else None)
@@ -279,7 +292,7 @@ def main():
         h.set_option("vec", args.vec)
     if args.order >= 0:
         h.set_option("order", args.order)
-    h.register_tables(tables, cfg.B)
+    h.register_tables(tables, cfg.B, pooling=args.pooling)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -331,7 +344,8 @@ def main():
         return float(t.item())
 
     # ---- fused (the product)
-    fused_step = lambda k: h.forward(d_in[k][0], d_in[k][1], stream)  # noqa: E731
+    fused_step = lambda k: h.forward(d_in[k][0], d_in[k][1], stream,  # noqa: E731
+                                     per_sample_weights=None if d_w is None else d_w[k])
     launches0 = h.query("kernel_launches")
     clk = ClockSampler(local)
     clk.start()
@@ -350,7 +364,8 @@ def main():
     # dominant kernel = the fused kernel (one launch per step); per-launch time from the same
     # events over the timed region
     nnz_mean = float(np.mean([mine[k % args.batches][0].size for k in range(args.steps)]))
-    hbm_b, tx_b = algorithmic_bytes(cfg, rank, nnz_mean)
+    hbm_b, tx_b = algorithmic_bytes(cfg, rank, nnz_mean, 4 if args.table_dtype == "f32" else 2,
+                                    args.weighted)
     peak_hbm, peak_src = measured_peaks()
     t_hbm = hbm_b / (peak_hbm * 1e9)
     t_nvl = tx_b / (NVLINK_GBS * 1e9)
@@ -387,6 +402,8 @@ def main():
     e2e = {"value": lookups / (e2e_total / 1e3), "unit": "lookups/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(b * h.G * h.D * 4),
            "ms_per_step": e2e_total / args.steps}
+    if args.weighted:
+        e2e["note"] = "forward_host has no per-sample-weight variant: e2e is the unweighted forward"
 
     # ---- unfused baseline: same pooling kernel -> staging, then NCCL all_to_all_single
     unfused = None
@@ -397,7 +414,8 @@ def main():
         final = torch.empty((b, cfg.G * cfg.D), dtype=torch.float32, device=dev)
 
         def unfused_step(k, permute):
-            h.pool_local(d_in[k][0], d_in[k][1], send, stream)
+            h.pool_local(d_in[k][0], d_in[k][1], send, stream,
+                         per_sample_weights=None if d_w is None else d_w[k])
             if shared:     # gloo: exchange through host memory (test mode only)
                 r_cpu = torch.empty(recv.numel(), dtype=recv.dtype)
                 dist.all_to_all_single(r_cpu, send.view(-1).cpu())
@@ -419,7 +437,7 @@ def main():
                                                     args.warmup))) / args.steps
         # parity of the two paths on the last batch (cheap, outside timing)
         k = 0
-        out_f = h.forward(d_in[k][0], d_in[k][1], stream).clone()
+        out_f = fused_step(k).clone()
         unfused_step(k, True)
         torch.cuda.synchronize()
         same = bool(torch.equal(out_f, final))
@@ -430,9 +448,9 @@ def main():
                    "fused_equals_unfused_bitwise": same}
 
     backward = None
-    if not args.no_backward:
+    if not args.no_backward and args.table_dtype == "f32":
         backward = backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared,
-                                    b2b_loop, max_over_ranks, peak_hbm, peak_src)
+                                    b2b_loop, max_over_ranks, peak_hbm, peak_src, d_w)
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
@@ -442,11 +460,14 @@ def main():
         "metric": "fused emb+All-to-All lookups/s (us/step in ms_per_step)",
         "value": value, "unit": "lookups/s", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "us_per_step": ms_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.table_dtype == "f32" else f"{args.table_dtype}-tables/f32-accumulate",
         "data": "synthetic (seeded Zipf indices, procedural fp32 tables; DESIGN.md Input recipe)",
         "config": {"workload": workload_desc(cfg), "global_batch": cfg.B,
                    "tables_per_rank": cfg.T[0], "rows": cfg.R, "dim": cfg.D,
                    "pooling": list(cfg.pool), "alpha": cfg.alpha, "world": N,
+                   "table_dtype": args.table_dtype, "pooling_mode": args.pooling,
+                   "per_sample_weights": bool(args.weighted),
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
                    "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
@@ -479,7 +500,7 @@ def main():
 
 
 def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b_loop,
-                     max_over_ranks, peak_hbm, peak_src):
+                     max_over_ranks, peak_hbm, peak_src, d_w=None):
     """f3: one training-step backward = sort plan of the batch's lookups + the
     fused backward kernel (gradient exchange DP -> MP over peer memory, segment reduce, sparse
     SGD on the tables).  Baseline: pack the owners' column blocks, NCCL all_to_all_single, then
@@ -492,17 +513,19 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
     gen.manual_seed(1234 + rank)
     grad = torch.randn((b, h.G * D), generator=gen, device=dev, dtype=torch.float32)
     lr = 1e-6
-    plan_step = lambda k: h.backward_plan(d_in[k][0], d_in[k][1], stream)  # noqa: E731
+    W_ = (lambda k: None) if d_w is None else (lambda k: d_w[k])  # noqa: E731
+    plan_step = lambda k: h.backward_plan(d_in[k][0], d_in[k][1], stream,  # noqa: E731
+                                          per_sample_weights=W_(k))
 
     def fused_step(k):
-        h.backward_plan(d_in[k][0], d_in[k][1], stream)
+        plan_step(k)
         h.backward(grad, lr, stream)
 
     send = torch.empty((N, b, T * D), dtype=torch.float32, device=dev)
     recv = torch.empty((cfg.B, T * D), dtype=torch.float32, device=dev)
 
     def unfused_step(k):
-        h.backward_plan(d_in[k][0], d_in[k][1], stream)
+        plan_step(k)
         send.copy_(grad.view(b, N, T * D).permute(1, 0, 2))      # owners' column blocks
         if shared:
             r_cpu = torch.empty(recv.numel(), dtype=recv.dtype)
@@ -517,7 +540,7 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
     step_ms = max_over_ranks(b2b_loop(fused_step, K, W)) / K
     launches = (h.query("kernel_launches") - l0) // (K + W)
     plan_ms = max_over_ranks(b2b_loop(plan_step, K, W)) / K
-    h.backward_plan(d_in[0][0], d_in[0][1], stream)
+    plan_step(0)
     kern_ms = max_over_ranks(b2b_loop(lambda k: h.backward(grad, lr, stream), K, W)) / K
     un_ms = max_over_ranks(b2b_loop(unfused_step, K, W)) / K
     # parity: fused vs unfused from the same tables on batch 0 (bitwise: same plan, same order)
