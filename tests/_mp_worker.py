@@ -73,6 +73,23 @@ def gpu_ipc_worker(rank, world, port, q):
     flags = h.read_flags()
     ok_flags = all(int(flags[src]) == 3 * oracle.signal_count(src, rank, cfg.T, cfg.part, 5)
                    for src in range(world))
+    # backward (f3) across processes: gradient rows pushed into the peer's IPC-mapped staging,
+    # counters across the process boundary; two steps against the oracle (integer gradients:
+    # every sum is exact, so the updated tables are bitwise equal)
+    rng = np.random.default_rng(77)
+    cur = [t.copy() for t in tabs_host]
+    ok_bwd = True
+    for step in range(2):
+        grads = [rng.integers(-4, 4, (int(cfg.part[s + 1] - cfg.part[s]), cfg.G * cfg.D))
+                 .astype(np.float32) for s in range(world)]
+        cur = oracle.backward_sgd(cfg.part, cfg.D, cfg.B, cfg.T, cur, [c[0] for c in csr],
+                                  [c[1] for c in csr], grads, -1.0)
+        h.backward_plan(idx, off)
+        h.backward(torch.from_numpy(grads[rank]).to(dev), -1.0)
+        torch.cuda.synchronize()
+        h.check()
+        for t in range(cfg.T[rank]):
+            ok_bwd &= bool(np.array_equal(mine[t].cpu().numpy(), cur[cfg.toff(rank) + t]))
     h.destroy()
-    q.put((rank, ok, ok_flags))
+    q.put((rank, ok and ok_bwd, ok_flags))
     dist.destroy_process_group()

@@ -38,6 +38,8 @@ def test_gloo_world2_bootstrap_and_rank_local_oracle_check():
 @pytest.mark.gpu
 def test_two_processes_one_gpu_cuda_ipc_path():
     """Each process maps the other's receive region with cudaIpcOpenMemHandle; fused forwards
-    (3 epochs) match the oracle bitwise and the arrival counters equal epoch * n(src->dst)."""
+    (3 epochs) match the oracle bitwise and the arrival counters equal epoch * n(src->dst); then
+    two fused backward steps (gradient rows pushed across the process boundary) update the
+    tables exactly as the oracle does."""
     for rank, ok, ok_flags in run(_mp_worker.gpu_ipc_worker, 2, timeout=300):
         assert ok and ok_flags, rank
