@@ -36,3 +36,5 @@ def test_bench_torchrun_shared_gpu(n):
     assert line["n_gpus"] == n and line["value"] > 0
     assert line["unfused"]["fused_equals_unfused_bitwise"] is True
     assert line["gpu_launches"] == 4
+    bwd = line["backward"]          # f3 across processes: fused exchange vs pack + all_to_all
+    assert bwd["fused_equals_unfused_bitwise"] is True and bwd["us_per_step"] > 0
