@@ -241,7 +241,7 @@ __device__ __forceinline__ void st_shared_f4(float* p, const float4& v) {
                : "memory");
 }
 template <int NVC, int MODE>
-__global__ void __launch_bounds__(128, NVC >= 8 ? 1 : 4) bwd_kernel(const __grid_constant__ BwdParams P) {
+__global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_kernel(const __grid_constant__ BwdParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_pushed[kMaxW];
   __shared__ float* s_tab[kMaxSmemTables];   // this rank's table pointers (T <= 256)
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : 4) bwd_kernel(const __grid
   // registers and applied in batches (all table-row loads in flight together).  The chunk's
   // first run, if it began in an earlier chunk, and its last run, if it goes on into the next
   // chunk, are left as partial sums in the chunk's two scratch slots for pass 2.
-  constexpr int UF = NVC >= 8 ? 1 : 8 / NVC;          // lookups in flight per lane
+  constexpr int UF = NVC >= 8 ? 1 : (NVC == 1 ? 4 : 8 / NVC);   // lookups in flight per lane
   int LPG = 1;
   while (LPG < DU && LPG < 32) LPG <<= 1;
   const int NG = 32 / LPG, grp = lane / LPG, gl = lane - grp * LPG;
