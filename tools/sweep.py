@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--B", type=int, default=0, help="override the global batch")
     ap.add_argument("--R", type=int, default=0, help="override rows per table")
     ap.add_argument("--P", type=int, default=0, help="override: fixed pooling factor")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"])
+    ap.add_argument("--weighted", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--flush-mode", default="write", choices=["write", "read", "sleep"])
     args = ap.parse_args()
@@ -48,9 +50,15 @@ def main():
     d_in = [(torch.from_numpy(i).to(dev), torch.from_numpy(o).to(dev)) for i, o in batches]
     nnz = np.mean([i.size for i, _ in batches])
     tables = sdev.rank_tables(cfg, 0, dev)
+    esize = 4
+    if args.dtype != "f32":
+        tables = [t.to({"bf16": torch.bfloat16, "f16": torch.float16}[args.dtype]) for t in tables]
+        esize = 2
+    d_w = [torch.from_numpy(synth.gen_weights(cfg, 0, i.size, batch=k)).to(dev)
+           for k, (i, _) in enumerate(batches)] if args.weighted else None
     flush = torch.zeros(128 << 20, dtype=torch.float32, device=dev)
     sink = torch.zeros((), device=dev)
-    hbm = nnz * cfg.D * 4 + nnz * 4 + (cfg.T[0] * cfg.B + 1) * 4 + cfg.B * cfg.G * cfg.D * 4
+    hbm = nnz * cfg.D * esize + nnz * (8 if args.weighted else 4) + (cfg.T[0] * cfg.B + 1) * 4 + cfg.B * cfg.G * cfg.D * 4
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     keys, vals = [], []
@@ -65,7 +73,7 @@ def main():
             for k, v in opts.items():
                 h.set_option(k, v)
             h.register_tables(tables, cfg.B)
-            h.forward(d_in[0][0], d_in[0][1])
+            h.forward(d_in[0][0], d_in[0][1], per_sample_weights=None if d_w is None else d_w[0])
         except Exception as e:   # invalid combination (e.g. too much shared memory)
             print(json.dumps({"config": cfg.name, "opts": opts, "error": str(e)[:200]}), flush=True)
             continue
@@ -91,7 +99,8 @@ def main():
             torch.cuda.synchronize()
             return np.array([a.elapsed_time(b) * 1e3 for a, b in ts])
 
-        us = run(lambda k: h.forward(d_in[k][0], d_in[k][1], st))
+        us = run(lambda k: h.forward(d_in[k][0], d_in[k][1], st,
+                                     per_sample_weights=None if d_w is None else d_w[k]))
         rec = {"config": cfg.name, "opts": opts, "grid": h.query("last_grid"),
                "us_p50": float(np.median(us)), "us_p10": float(np.percentile(us, 10)),
                "us_p90": float(np.percentile(us, 90)), "us_mean": float(us.mean()),
