@@ -571,6 +571,7 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
             "roofline": {"bound": "hbm", "kernel": "bwd_kernel", "achieved": alg / kern_s / 1e9,
                          "peak": peak_hbm, "unit": "GB/s", "peak_source": peak_src,
                          "frac": alg / kern_s / 1e9 / peak_hbm, "algorithmic_bytes": int(alg),
+                         "traffic": ncu_traffic(cfg, "_backward"),
                          "distinct_rows": int(uniq), "nvlink_tx_bytes": int(tx)}}
 
 
@@ -582,7 +583,7 @@ def working_set_mb(cfg, idx, off):
     return (idx.size * 4 + off.size * 4 + rows * cfg.D * 4) / 1e6
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, suffix=""):
     """DRAM bytes per fused launch from a committed ncu --set full capture, if one exists for
     this workload (profiles/ncu_traffic.json written from the .ncu-rep by tools)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -590,7 +591,7 @@ def ncu_traffic(cfg):
         return None
     with open(p) as f:
         d = json.load(f)
-    key = f"{cfg.name}_W{cfg.W}"
+    key = f"{cfg.name}_W{cfg.W}{suffix}"
     v = d.get(key)
     return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
 
