@@ -383,7 +383,10 @@ def main():
     roof = roofline(ms_step / 1e3)
     roof["algorithmic_bytes_per_launch"] = hbm_b
     roof["nvlink_tx_bytes_per_launch"] = tx_b
-    roof["traffic"] = ncu_traffic(cfg)
+    # the committed capture is of the default variant (fp32 sum, unweighted, default alpha)
+    default_variant = (args.table_dtype == "f32" and args.pooling == "sum" and not args.weighted
+                       and args.alpha == 1.05)
+    roof["traffic"] = ncu_traffic(cfg) if default_variant else None
     roof["roofline_us"] = max(t_hbm, t_nvl) * 1e6
     flushed = {"us_per_step": flushed_total / args.steps * 1e3,
                "us_p50": float(np.median(ms)) * 1e3, "us_p90": float(np.percentile(ms, 90)) * 1e3,
@@ -571,7 +574,8 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
             "roofline": {"bound": "hbm", "kernel": "bwd_kernel", "achieved": alg / kern_s / 1e9,
                          "peak": peak_hbm, "unit": "GB/s", "peak_source": peak_src,
                          "frac": alg / kern_s / 1e9 / peak_hbm, "algorithmic_bytes": int(alg),
-                         "traffic": ncu_traffic(cfg, "_backward"),
+                         "traffic": ncu_traffic(cfg, "_backward") if (
+                             d_w is None and args.pooling == "sum" and args.alpha == 1.05) else None,
                          "distinct_rows": int(uniq), "nvlink_tx_bytes": int(tx)}}
 
 
