@@ -122,8 +122,11 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
 
 /* The same forward fed from HOST memory (the end-to-end path): copies h_indices / h_offsets
  * (host, ideally pinned) into library-owned device staging, runs the fused forward, and copies
- * the [b_r][G*D] float32 result into h_out (host, b_r*G*D floats), all enqueued on `stream`.
- * Returns after enqueuing; synchronise the stream before reading h_out (collective). */
+ * the [b_r][G*D] float32 result into h_out (host, b_r*G*D floats).  The forward and the result
+ * copy are enqueued on `stream`; the input copy runs on a library-owned copy stream that
+ * `stream` waits for, into one of two staging buffers, so consecutive calls overlap the next
+ * call's host->device copy with this call's device->host copy.  Returns after enqueuing;
+ * synchronise the stream before reading h_out or reusing h_indices / h_offsets (collective). */
 int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
                          int64_t num_indices, void* stream, float* h_out);
 

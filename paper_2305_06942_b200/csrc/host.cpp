@@ -108,9 +108,14 @@ struct emb_a2a {
   int* d_err = nullptr;
   int* h_verr = nullptr;                 // validate error word (mapped)
   int* d_verr = nullptr;
-  int32_t* d_idx_stage = nullptr;
-  int32_t* d_off_stage = nullptr;
+  // forward_host: double-buffered input staging filled on a copy stream, so the next call's
+  // host->device copy overlaps this call's device->host copy (different copy engines)
+  int32_t* d_idx_stage[2] = {nullptr, nullptr};
+  int32_t* d_off_stage[2] = {nullptr, nullptr};
   size_t idx_stage_cap = 0, off_stage_cap = 0;
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_free[2] = {nullptr, nullptr};
+  uint64_t host_calls = 0;
 
   uint64_t epoch = 0;
   uint64_t barrier_epoch = 0;
@@ -204,8 +209,12 @@ void release_registration(emb_a2a* h) {
   if (h->d_trace) cudaFree(h->d_trace);
   h->d_trace = nullptr;
   h->d_slice_cnt = nullptr;
-  if (h->d_idx_stage) cudaFree(h->d_idx_stage);
-  if (h->d_off_stage) cudaFree(h->d_off_stage);
+  for (int x = 0; x < 2; ++x) {
+    if (h->d_idx_stage[x]) cudaFree(h->d_idx_stage[x]);
+    if (h->d_off_stage[x]) cudaFree(h->d_off_stage[x]);
+    h->d_idx_stage[x] = nullptr;
+    h->d_off_stage[x] = nullptr;
+  }
   for (int x = 0; x < 2; ++x) {
     if (h->d_keys[x]) cudaFree(h->d_keys[x]);
     if (h->d_bags[x]) cudaFree(h->d_bags[x]);
@@ -233,8 +242,6 @@ void release_registration(emb_a2a* h) {
   h->d_tables = nullptr;
   h->d_rows = nullptr;
   h->d_done = nullptr;
-  h->d_idx_stage = nullptr;
-  h->d_off_stage = nullptr;
   h->idx_stage_cap = h->off_stage_cap = 0;
   h->flags = nullptr;
   h->recv[0] = h->recv[1] = nullptr;
@@ -727,30 +734,50 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
   cudaStream_t st = (cudaStream_t)stream;
   const size_t nidx = (size_t)std::max<int64_t>(num_indices, 1);
   const size_t noff = (size_t)h->T * h->B + 1;
-  if (nidx > h->idx_stage_cap) {
-    if (h->d_idx_stage) cudaFree(h->d_idx_stage);
-    h->d_idx_stage = nullptr;
-    h->idx_stage_cap = 0;
-    CUDA_TRY(h, cudaMalloc((void**)&h->d_idx_stage, nidx * sizeof(int32_t)));
-    h->idx_stage_cap = nidx;
+  if (!h->h2d_stream) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    for (int x = 0; x < 2; ++x)
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_free[x], cudaEventDisableTiming));
   }
-  if (noff > h->off_stage_cap) {
-    if (h->d_off_stage) cudaFree(h->d_off_stage);
-    h->d_off_stage = nullptr;
-    h->off_stage_cap = 0;
-    CUDA_TRY(h, cudaMalloc((void**)&h->d_off_stage, noff * sizeof(int32_t)));
-    h->off_stage_cap = noff;
+  // grow-only with headroom: batches vary in size, and cudaFree synchronises the device
+  if (nidx > h->idx_stage_cap || noff > h->off_stage_cap) {
+    // a regrow waits for earlier calls' copies and forwards (the first call has nothing to
+    // wait for -- and must not wait: loopback peers' forwards may still be in flight)
+    if (h->idx_stage_cap > 0) CUDA_TRY(h, cudaDeviceSynchronize());
+    const size_t icap = std::max(h->idx_stage_cap, nidx + nidx / 4);
+    const size_t ocap = std::max(h->off_stage_cap, noff);
+    for (int x = 0; x < 2; ++x) {
+      if (h->d_idx_stage[x]) cudaFree(h->d_idx_stage[x]);
+      if (h->d_off_stage[x]) cudaFree(h->d_off_stage[x]);
+      h->d_idx_stage[x] = nullptr;
+      h->d_off_stage[x] = nullptr;
+    }
+    h->idx_stage_cap = h->off_stage_cap = 0;
+    for (int x = 0; x < 2; ++x) {
+      CUDA_TRY(h, cudaMalloc((void**)&h->d_idx_stage[x], icap * sizeof(int32_t)));
+      CUDA_TRY(h, cudaMalloc((void**)&h->d_off_stage[x], ocap * sizeof(int32_t)));
+    }
+    h->idx_stage_cap = icap;
+    h->off_stage_cap = ocap;
   }
+  const int par = (int)(h->host_calls++ & 1);
+  // staging[par] was last read by the forward two calls ago (ev_free[par]); the copy stream
+  // does not wait for this stream's device->host copy of the previous call
+  CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_free[par], 0));
   if (num_indices > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(h->d_idx_stage, h_indices, num_indices * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_idx_stage[par], h_indices, num_indices * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, h->h2d_stream));
   if (h->T > 0 && h->B > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(h->d_off_stage, h_offsets, noff * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_off_stage[par], h_offsets, noff * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, h->h2d_stream));
+  CUDA_TRY(h, cudaEventRecord(h->ev_in, h->h2d_stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_in, 0));
   float* dout = nullptr;
-  rc = emb_a2a_forward(h, h->d_idx_stage, h->d_off_stage, num_indices, stream, &dout, nullptr,
-                       nullptr);
+  rc = emb_a2a_forward(h, h->d_idx_stage[par], h->d_off_stage[par], num_indices, stream, &dout,
+                       nullptr, nullptr);
   if (rc) return rc;
+  CUDA_TRY(h, cudaEventRecord(h->ev_free[par], st));
   const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
   if (out_bytes) CUDA_TRY(h, cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
   return EMB_A2A_OK;
@@ -1264,6 +1291,10 @@ int emb_a2a_destroy(emb_a2a_t* h) {
       release_registration(h);
     }
     if (h->h_err) cudaFreeHost(h->h_err);
+    if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
+    if (h->ev_in) cudaEventDestroy(h->ev_in);
+    for (int x = 0; x < 2; ++x)
+      if (h->ev_free[x]) cudaEventDestroy(h->ev_free[x]);
   }
   delete h;
   return rc;

@@ -325,6 +325,34 @@ def test_forward_host_end_to_end():
     g.destroy()
 
 
+def test_forward_host_back_to_back_double_buffered_staging():
+    """Six forward_host calls without a sync in between (inputs of different sizes, so the
+    staging regrows once; the two staging buffers alternate and each call's input copy runs on
+    the copy stream while the previous call's result copy is in flight): every result exact."""
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    probs = [random_problem(900 + k, W=1, value_mode=1, max_B=128, max_D=64) for k in range(3)]
+    p0 = probs[0]
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    h.register_tables([torch.from_numpy(t).to(dev()) for t in p0.tables], p0.B)
+    R = [t.shape[0] for t in p0.tables]
+    rng = np.random.default_rng(5)
+    cases = []
+    for k in range(6):   # same tables / B / D, new bags each call; call 3 is much larger
+        L = 40 if k == 3 else 6
+        bags = [[list(rng.integers(0, R[t], rng.integers(0, L))) for _ in range(p0.B)]
+                for t in range(len(p0.tables))]
+        i, o = csr_from_bags(bags)
+        cases.append((torch.from_numpy(i).pin_memory(), torch.from_numpy(o).pin_memory(),
+                      torch.empty((p0.B, p0.G * p0.D), dtype=torch.float32).pin_memory(), i, o))
+    for hi, ho, out, _, _ in cases:
+        h.forward_host(hi, ho, out)
+    torch.cuda.synchronize()
+    for _, _, out, i, o in cases:
+        ref = oracle.emb_a2a(p0.part, p0.D, p0.B, p0.T, p0.tables, [i], [o])
+        np.testing.assert_array_equal(out.numpy(), ref[0])
+    h.destroy()
+
+
 # ---------------------------------------------------------------------------- full size, sampled
 
 def test_device_fill_equals_oracle_generator():
