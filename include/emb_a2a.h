@@ -130,6 +130,17 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
 int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
                          int64_t num_indices, void* stream, float* h_out);
 
+/* A sequence of nsteps host-buffer forwards, pipelined (collective; every rank passes the same
+ * nsteps): step k copies h_indices[k] (num_indices[k] int32) and h_offsets[k] (T_r*B+1 int32)
+ * in on one library copy stream, runs the fused forward on `stream`, and copies the result into
+ * h_out[k] (b_r*G*D float32) on a second copy stream -- so step k's result copy overlaps step
+ * k+1's forward and step k+2's input copy (the serving loop).  All host buffers ideally pinned,
+ * and left untouched until `stream` is synchronised; `stream` completes only after the last
+ * result copy.  Returns after enqueuing. */
+int emb_a2a_forward_host_batch(emb_a2a_t* h, int nsteps, const int32_t* const* h_indices,
+                               const int32_t* const* h_offsets, const int64_t* num_indices,
+                               float* const* h_out, void* stream);
+
 /* Unfused baseline, first half (not collective): the same pooling, written with local stores to
  * a caller-owned DEVICE staging buffer `send`, dest-major [W][b_s][T_r][D] float32 (the block of
  * destination s starts at p_s*T_r*D floats).  The second half is the caller's NCCL

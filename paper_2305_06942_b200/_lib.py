@@ -41,6 +41,7 @@ _SIGS = {
     "emb_a2a_forward": (_I, [_P, _P, _P, _I64, _P, ctypes.POINTER(_P), _PI64, _PI64]),
     "emb_a2a_forward_weighted": (_I, [_P, _P, _P, _P, _I64, _P, ctypes.POINTER(_P), _PI64, _PI64]),
     "emb_a2a_forward_host": (_I, [_P, _P, _P, _I64, _P, _P]),
+    "emb_a2a_forward_host_batch": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "emb_a2a_pool_local": (_I, [_P, _P, _P, _I64, _P, _P]),
     "emb_a2a_pool_local_weighted": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
     "emb_a2a_backward_plan": (_I, [_P, _P, _P, _P, _I64, _P]),

@@ -113,8 +113,9 @@ struct emb_a2a {
   int32_t* d_idx_stage[2] = {nullptr, nullptr};
   int32_t* d_off_stage[2] = {nullptr, nullptr};
   size_t idx_stage_cap = 0, off_stage_cap = 0;
-  cudaStream_t h2d_stream = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   uint64_t host_calls = 0;
 
   uint64_t epoch = 0;
@@ -720,25 +721,23 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
   return EMB_A2A_OK;
 }
 
-int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
-                         int64_t num_indices, void* stream, float* h_out) {
-  if (!h) return EMB_A2A_EINVAL;
-  int rc = check_async(h);
-  if (rc) return rc;
-  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "forward_host before register_tables");
-  if (num_indices < 0 || num_indices >= (1ll << 31))
-    return fail(h, EMB_A2A_EINVAL, "num_indices out of range");
-  if (!h_out || (!h_offsets && h->T > 0 && h->B > 0) || (num_indices > 0 && !h_indices))
-    return fail(h, EMB_A2A_EINVAL, "host buffers are NULL");
-  DeviceGuard guard(h->dev);
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+
+// forward_host plumbing: copy streams, events, double-buffered input staging (grow-only).
+int host_staging(emb_a2a* h, int64_t num_indices) {
   const size_t nidx = (size_t)std::max<int64_t>(num_indices, 1);
   const size_t noff = (size_t)h->T * h->B + 1;
   if (!h->h2d_stream) {
     CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
     CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < 2; ++x) {
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_free[x], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_done[x], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_out[x], cudaEventDisableTiming));
+    }
   }
   // grow-only with headroom: batches vary in size, and cudaFree synchronises the device
   if (nidx > h->idx_stage_cap || noff > h->off_stage_cap) {
@@ -761,6 +760,30 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
     h->idx_stage_cap = icap;
     h->off_stage_cap = ocap;
   }
+  return EMB_A2A_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* h_offsets,
+                         int64_t num_indices, void* stream, float* h_out) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "forward_host before register_tables");
+  if (num_indices < 0 || num_indices >= (1ll << 31))
+    return fail(h, EMB_A2A_EINVAL, "num_indices out of range");
+  if (!h_out || (!h_offsets && h->T > 0 && h->B > 0) || (num_indices > 0 && !h_indices))
+    return fail(h, EMB_A2A_EINVAL, "host buffers are NULL");
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = host_staging(h, num_indices);
+  if (rc) return rc;
+  const size_t noff = (size_t)h->T * h->B + 1;
+  {
+  }
   const int par = (int)(h->host_calls++ & 1);
   // staging[par] was last read by the forward two calls ago (ev_free[par]); the copy stream
   // does not wait for this stream's device->host copy of the previous call
@@ -780,6 +803,64 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
   CUDA_TRY(h, cudaEventRecord(h->ev_free[par], st));
   const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
   if (out_bytes) CUDA_TRY(h, cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_forward_host_batch(emb_a2a_t* h, int nsteps, const int32_t* const* h_indices,
+                               const int32_t* const* h_offsets, const int64_t* num_indices,
+                               float* const* h_out, void* stream) {
+  if (!h) return EMB_A2A_EINVAL;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "forward_host_batch before register_tables");
+  if (nsteps < 0 || (nsteps > 0 && (!h_indices || !h_offsets || !num_indices || !h_out)))
+    return fail(h, EMB_A2A_EINVAL, "bad step arrays");
+  int64_t nmax = 0;
+  for (int k = 0; k < nsteps; ++k) {
+    if (num_indices[k] < 0 || num_indices[k] >= (1ll << 31))
+      return fail(h, EMB_A2A_EINVAL, "num_indices[%d] out of range", k);
+    if (!h_out[k] || (!h_offsets[k] && h->T > 0 && h->B > 0) ||
+        (num_indices[k] > 0 && !h_indices[k]))
+      return fail(h, EMB_A2A_EINVAL, "host buffers of step %d are NULL", k);
+    nmax = std::max(nmax, num_indices[k]);
+  }
+  DeviceGuard guard(h->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = host_staging(h, nmax);
+  if (rc) return rc;
+  const size_t noff = (size_t)h->T * h->B + 1;
+  const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
+  for (int k = 0; k < nsteps; ++k) {
+    const int par = (int)(h->host_calls++ & 1);
+    // inputs: copy stream, into the staging the forward two steps ago has finished reading
+    CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_free[par], 0));
+    if (num_indices[k] > 0)
+      CUDA_TRY(h, cudaMemcpyAsync(h->d_idx_stage[par], h_indices[k],
+                                  num_indices[k] * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                  h->h2d_stream));
+    if (h->T > 0 && h->B > 0)
+      CUDA_TRY(h, cudaMemcpyAsync(h->d_off_stage[par], h_offsets[k], noff * sizeof(int32_t),
+                                  cudaMemcpyHostToDevice, h->h2d_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_in, h->h2d_stream));
+    // forward on `stream`, once the inputs are in and the receive buffer it will write (the
+    // one of two steps ago) has been copied out
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_in, 0));
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_out[(h->epoch + 1) & 1], 0));
+    float* dout = nullptr;
+    rc = emb_a2a_forward(h, h->d_idx_stage[par], h->d_off_stage[par], num_indices[k], stream,
+                         &dout, nullptr, nullptr);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_free[par], st));
+    CUDA_TRY(h, cudaEventRecord(h->ev_done[h->epoch & 1], st));
+    // result: device->host on the other copy stream, overlapping the next step's forward
+    CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_done[h->epoch & 1], 0));
+    if (out_bytes)
+      CUDA_TRY(h, cudaMemcpyAsync(h_out[k], dout, out_bytes, cudaMemcpyDeviceToHost,
+                                  h->d2h_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_out[h->epoch & 1], h->d2h_stream));
+  }
+  // `stream` completes only after every result copy
+  for (int x = 0; x < 2; ++x) CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_out[x], 0));
   return EMB_A2A_OK;
 }
 
@@ -1292,9 +1373,13 @@ int emb_a2a_destroy(emb_a2a_t* h) {
     }
     if (h->h_err) cudaFreeHost(h->h_err);
     if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
+    if (h->d2h_stream) cudaStreamDestroy(h->d2h_stream);
     if (h->ev_in) cudaEventDestroy(h->ev_in);
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < 2; ++x) {
       if (h->ev_free[x]) cudaEventDestroy(h->ev_free[x]);
+      if (h->ev_done[x]) cudaEventDestroy(h->ev_done[x]);
+      if (h->ev_out[x]) cudaEventDestroy(h->ev_out[x]);
+    }
   }
   delete h;
   return rc;

@@ -259,6 +259,28 @@ class EmbA2A:
         """Raise if an asynchronous device failure (a wait timeout) was recorded."""
         self._err(lib.emb_a2a_check(self._h), "emb_a2a_check")
 
+    def forward_host_batch(self, indices: Sequence[torch.Tensor], offsets: Sequence[torch.Tensor],
+                           outs: Sequence[torch.Tensor], stream=None) -> None:
+        """Pipelined sequence of host-buffer forwards (collective): step k reads host int32
+        indices[k] / offsets[k] and writes host float32 outs[k] [b_r, G*D]; the copies of
+        neighbouring steps overlap the forwards.  Synchronise `stream` before reading outs."""
+        n = len(indices)
+        if not (len(offsets) == n and len(outs) == n):
+            raise ValueError("indices, offsets and outs must have one entry per step")
+        for k in range(n):
+            for t, dt, nm in ((indices[k], torch.int32, "indices"), (offsets[k], torch.int32, "offsets"),
+                              (outs[k], torch.float32, "outs")):
+                if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous():
+                    raise ValueError(f"{nm}[{k}] must be a contiguous host {dt} tensor")
+        P = ctypes.c_void_p * max(n, 1)
+        ip = P(*[t.data_ptr() if t.numel() else None for t in indices])
+        op = P(*[t.data_ptr() for t in offsets])
+        outp = P(*[t.data_ptr() for t in outs])
+        nn = (ctypes.c_int64 * max(n, 1))(*[t.numel() for t in indices])
+        rc = lib.emb_a2a_forward_host_batch(self._h, n, ip, op, nn, outp,
+                                            _stream_ptr(stream, self.device))
+        self._err(rc, "emb_a2a_forward_host_batch")
+
     def device_barrier(self, stream=None) -> None:
         """Collective: the stream waits on the device until every rank has arrived."""
         self._err(lib.emb_a2a_device_barrier(self._h, _stream_ptr(stream, self.device)),

@@ -350,6 +350,16 @@ def test_forward_host_back_to_back_double_buffered_staging():
     for _, _, out, i, o in cases:
         ref = oracle.emb_a2a(p0.part, p0.D, p0.B, p0.T, p0.tables, [i], [o])
         np.testing.assert_array_equal(out.numpy(), ref[0])
+        out.zero_()
+    # the pipelined batch API over the same six steps, twice (receive buffers and staging
+    # alternate; result copies overlap the next forward)
+    for rep in range(2):
+        h.forward_host_batch([c[0] for c in cases], [c[1] for c in cases], [c[2] for c in cases])
+        torch.cuda.synchronize()
+        for _, _, out, i, o in cases:
+            ref = oracle.emb_a2a(p0.part, p0.D, p0.B, p0.T, p0.tables, [i], [o])
+            np.testing.assert_array_equal(out.numpy(), ref[0])
+            out.zero_()
     h.destroy()
 
 
