@@ -276,6 +276,37 @@ def test_empty_plan_and_empty_blocks():
     run.destroy()
 
 
+def test_rank_without_tables_and_uneven_tables():
+    """W=3, T = [2, 0, 3], ragged partition: the rank without tables still pushes its gradient
+    rows to the owners; every owner's tables match the oracle bitwise (exact-int)."""
+    rng = np.random.default_rng(11)
+    D, B = 12, 30
+    T = [2, 0, 3]
+    part = np.array([0, 7, 19, 30])
+    R = [17, 5, 23, 9, 40]
+    tables = [rng.integers(-8, 8, (r, D)).astype(np.float32) for r in R]
+    idx, off = [], []
+    g = 0
+    for r in range(3):
+        bags = []
+        for t in range(T[r]):
+            bags.append([list(rng.integers(0, R[g], rng.integers(0, 9))) for _ in range(B)])
+            g += 1
+        i, o = csr_from_bags(bags) if bags else (np.zeros(0, np.int32), np.zeros(1, np.int32))
+        idx.append(i)
+        off.append(o)
+    p = Problem(3, T, D, B, part, tables, idx, off)
+    grads = grads_for(p, 4, 1)
+    want = oracle.backward_sgd(p.part, D, B, T, p.tables, p.indices, p.offsets, grads, -1.0)
+    run = Run(p)
+    for step in range(2):
+        run.backward(grads, -1.0)
+        for a, b in zip(run.tables(), want):
+            np.testing.assert_array_equal(a, b)
+        want = oracle.backward_sgd(p.part, D, B, T, want, p.indices, p.offsets, grads, -1.0)
+    run.destroy()
+
+
 def test_backward_rejects_half_tables_and_missing_plan():
     from paper_2305_06942_b200 import EmbA2A, LocalGroup
     from paper_2305_06942_b200.emb_a2a import EmbA2AError
