@@ -227,6 +227,18 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
 }
 
 // ------------------------------------------------------------------------- fused backward
+// Per-warp timeline of the backward (the "trace" option; read with emb_a2a_read_trace): record
+// (warp << 40 | event << 32 | payload, %globaltimer).  Events: 20 warp start, 21 exchange done,
+// 22 chunk start (payload = chunk), 23 chunk keys in, 24 sub-batch staged, 25 sub-batch done,
+// 26 warp done.  Lane 0 only.
+__device__ __forceinline__ void btrace(const BwdParams& P, unsigned event, unsigned payload) {
+  if (P.trace == nullptr || (threadIdx.x & 31) != 0) return;
+  const unsigned long long i = atomicAdd(P.trace, 1ull);
+  if ((long long)i >= P.trace_cap) return;
+  P.trace[2 + 2 * i] = ((unsigned long long)(blockIdx.x * 32 + (threadIdx.x >> 5)) << 40) |
+                       ((unsigned long long)event << 32) | payload;
+  P.trace[3 + 2 * i] = globaltimer();
+}
 // Sparse SGD step on 4 elements (R#29): w = fl(w - fl(lr * g)).
 __device__ __forceinline__ void sgd4(float4& w, float lr, const float4& g) {
   w.x = __fsub_rn(w.x, __fmul_rn(lr, g.x));
@@ -249,6 +261,7 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int D = P.D, DU = D >> 2;
 
+  btrace(P, 20, 0);
   // ---- exchange (fused, W > 1): push this rank's gradient rows to their table owners
   if (P.fused && P.W > 1) {
     for (int q = tid; q < P.W; q += blockDim.x) s_pushed[q] = 0u;
@@ -339,16 +352,11 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   const unsigned B32 = (unsigned)P.B;
   const unsigned* __restrict__ keys = P.keys;
 
-  (void)gw;
-  (void)nwt;
-  while (true) {
-    // chunks handed out by ticket (P.ticket zeroed before the launch): a warp that drew
-    // cheap chunks takes more
-    if (lane == 0) s_ticket[warp] = (long long)atomicAdd(P.ticket, 1u);
-    __syncwarp();
-    const long long c = s_ticket[warp];
-    __syncwarp();
-    if (c >= P.nchunks) break;
+  // chunk gw first (no atomic), then further chunks by ticket (P.ticket zeroed before the
+  // launch), so a warp that drew cheap chunks takes more
+  btrace(P, 21, 0);
+  for (long long c = gw; c < P.nchunks;) {
+    btrace(P, 22, (unsigned)c);
     const long long p0 = c * kBwdChunk;
     const int clen = (n - p0) < kBwdChunk ? (int)(n - p0) : kBwdChunk;
     // sub-batch 0's lookups; the keys just before and just after the chunk
@@ -365,6 +373,7 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
     }
     cf = __shfl_sync(kFull, cf, 0);
     const bool chunk_in = cf & 1, chunk_out = cf & 2;
+    btrace(P, 23, 0);
     bool ob = chunk_in;          // the run entering the current sub-batch began before the chunk
     unsigned prev_last = 0u;     // last key of the previous sub-batch
     const int nsb = (clen + 31) / 32;
@@ -388,10 +397,11 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
       const int npieces = __popc(startm);
       __syncwarp();                                  // the previous sub-batch's readers are done
       if (lane < len) {
-        const unsigned t = (unsigned)bag / B32;
+        const unsigned t = P.rbits >= 32 ? 0u : key >> P.rbits;   // bag = t * B + j
         const long long j = (long long)((unsigned)bag - t * B32);
         int s = 0;
-        while (P.part[s + 1] <= j) ++s;              // destination of bag j
+        if (P.W > 1)
+          while (P.part[s + 1] <= j) ++s;            // destination of bag j
         const float* src;
         if (P.fused)
           src = (s == P.r) ? P.grad + ((j - pr) * P.G + P.toff + (int)t) * D
@@ -513,6 +523,7 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
         acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         cur_w[v] = acc[v];
       }
+      btrace(P, 24, (unsigned)sb);
       if (npieces == 1 && NG > 1) {
         // one run fills the sub-batch (a Zipf-hot row): every lane group sums an equal share of
         // its lookups, then the shares are added in group order (after the carried-in sum)
@@ -558,8 +569,14 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
       prev_last = keyl;
       key = nkey;
       bag = nbag;
+      btrace(P, 25, (unsigned)sb);
     }
+    if (lane == 0) s_ticket[warp] = nwt + (long long)atomicAdd(P.ticket, 1u);
+    __syncwarp();
+    c = s_ticket[warp];
+    __syncwarp();
   }
+  btrace(P, 26, 0);
 }
 
 // ---- reduce + update, pass 2 (R#31): the runs that cross chunk boundaries.  The chunk a run

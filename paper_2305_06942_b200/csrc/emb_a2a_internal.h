@@ -201,6 +201,8 @@ struct BwdParams {
   float* scratch;              // [nchunks][2][D] partial sums of runs crossing chunk edges
   unsigned char* info;         // [nchunks] bit 0: owns a crossing run, bit 1: inside one
   unsigned* ticket;            // pass-1 chunk tickets (zeroed before each launch)
+  unsigned long long* trace;   // optional %globaltimer event log (the "trace" option), NULL = off
+  long long trace_cap;
   int* err;
   long long n;                 // lookups in the plan
   long long B, timeout_ns;

@@ -941,6 +941,8 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.scratch = h->d_scratch;
   P.info = h->d_info;
   P.ticket = h->d_hist + kMaxPasses * 256 + kMaxPasses;
+  P.trace = h->d_trace;
+  P.trace_cap = h->trace_cap;
   P.err = h->d_err;
   P.n = h->planned ? h->plan_n : 0;
   P.B = h->B;
