@@ -38,11 +38,6 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -50,6 +45,13 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long
 }
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Programmatic dependent launch: the next kernel on the stream may be scheduled while this one
+// drains (launch_dependents); a kernel waits (griddepcontrol.wait) for its predecessor's grid
+// to complete -- and its writes to be visible -- before it reads anything the predecessor wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void st_f4(float* p, const float4& v) {
   asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -135,7 +137,9 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   __shared__ unsigned s_warp[NW];
   __shared__ unsigned s_tile;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_trigger();
   for (int i = tid; i < NW * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
+  pdl_wait();
   if (tid == 0) s_tile = atomicAdd(P.tile_ctr, 1u);
   __syncthreads();
   const long long tile = s_tile;
@@ -261,6 +265,8 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int D = P.D, DU = D >> 2;
 
+  pdl_wait();     // the plan (sort) and the caller's gradient are complete
+  pdl_trigger();
   btrace(P, 20, 0);
   // ---- exchange (fused, W > 1): push this rank's gradient rows to their table owners
   if (P.fused && P.W > 1) {
@@ -588,6 +594,9 @@ __global__ void __launch_bounds__(256) bwd_fold_kernel(const __grid_constant__ B
   const int lane = threadIdx.x & 31;
   const int D = P.D, DU = D >> 2;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  pdl_wait();     // pass 1 complete: partials, info
+  pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.ticket = 0u;   // pass 1's tickets, for next time
   const unsigned rmask = P.rbits >= 32 ? 0xffffffffu : ((1u << P.rbits) - 1u);
   constexpr int BATCH = NVC >= 16 ? 1 : 16 / NVC;
   for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < P.nchunks;
@@ -671,6 +680,21 @@ BwdFn pick_fold(const BwdParams& P) {
        : nvc <= 4 ? bwd_fold_kernel<4> : bwd_fold_kernel<8>;
 }
 
+cudaError_t launch_pdl(const void* fn, unsigned grid, int threads, size_t smem, cudaStream_t st,
+                       void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 size_t bwd_smem(const BwdParams& P, int threads) {
   return (size_t)(threads / 32) * (size_t)P.wbytes;
 }
@@ -686,11 +710,11 @@ cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int 
     if (e != cudaSuccess) return e;
   }
   for (int p = 0; p < npasses; ++p) {
-    if (passes[p].wts_in)
-      bwd_onesweep_kernel<true><<<(unsigned)ntiles, kSortThreads, 0, st>>>(passes[p]);
-    else
-      bwd_onesweep_kernel<false><<<(unsigned)ntiles, kSortThreads, 0, st>>>(passes[p]);
-    cudaError_t e = cudaGetLastError();
+    PassParams pp = passes[p];
+    void* args[] = {&pp};
+    const void* fn = passes[p].wts_in ? reinterpret_cast<const void*>(bwd_onesweep_kernel<true>)
+                                      : reinterpret_cast<const void*>(bwd_onesweep_kernel<false>);
+    cudaError_t e = launch_pdl(fn, (unsigned)ntiles, kSortThreads, 0, st, args);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -731,14 +755,17 @@ cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size
   BwdFn fn = pick_bwd(P);
   BwdParams Pc = P;
   void* args[] = {&Pc};
-  cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(threads),
-                                   args, smem, st);
+  cudaError_t e = launch_pdl(reinterpret_cast<const void*>(fn), grid, threads, smem, st, args);
   if (e != cudaSuccess || P.T == 0 || P.nchunks == 0) return e;
   // pass 2: one warp per chunk (most exit at once)
   const long long blocks = (P.nchunks + 7) / 8;
   const unsigned g2 = (unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16);
   BwdFn f2 = pick_fold(P);
-  return cudaLaunchKernel(reinterpret_cast<const void*>(f2), dim3(g2), dim3(256), args, 0, st);
+  // pass 2 overlaps pass 1's drain only when this rank has the GPU to itself: with virtual
+  // ranks sharing one device, its early CTAs could take the slots a peer's pass 1 still needs
+  if (!P.pdl_fold) return cudaLaunchKernel(reinterpret_cast<const void*>(f2), dim3(g2), dim3(256),
+                                           args, 0, st);
+  return launch_pdl(reinterpret_cast<const void*>(f2), g2, 256, 0, st, args);
 }
 
 }  // namespace emba2a

@@ -212,6 +212,7 @@ struct BwdParams {
   long long wbytes;            // shared memory per warp (finish queue)
   int flist;                   // finish-queue entries per warp
   int W, r, T, D, G, toff, rbits, fused, mean, parity;
+  int pdl_fold;                // launch pass 2 with programmatic dependent launch
   long long part[kMaxW + 1];
   int allT[kMaxW];
   int tofs[kMaxW];

@@ -979,8 +979,8 @@ int run_backward(emb_a2a* h, BwdParams& P, cudaStream_t st) {
     if (e != cudaSuccess) return fail(h, EMB_A2A_ECUDA, "backward plan: %s", cudaGetErrorString(e));
     h->bwd_mode = mode;
   }
-  if (P.T > 0 && P.n > 0)
-    CUDA_TRY(h, cudaMemsetAsync(P.ticket, 0, sizeof(unsigned), st));
+  // P.ticket: zero when allocated, reset by pass 2 of each launch (no memset between kernels)
+  P.pdl_fold = (h->bwd_share <= 1) ? 1 : 0;
   cudaError_t e = launch_backward(P, h->bwd_grid, (int)h->bwd_threads, h->bwd_smem, st);
   if (e != cudaSuccess) {
     h->poisoned = true;
@@ -1046,7 +1046,10 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     h->wts_cap = ncap;
   }
   // [pass histograms | pass tile tickets | backward chunk ticket]
-  if (!h->d_hist && (rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses + 1))) return rc;
+  if (!h->d_hist) {
+    if ((rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses + 1))) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (kMaxPasses * 256 + kMaxPasses + 1) * 4, st));
+  }
   const size_t nstatus = (size_t)passes * ntiles * 256;
   if (nstatus > h->status_cap) {
     const size_t scap = nstatus + nstatus / 4 + 4 * 256;
