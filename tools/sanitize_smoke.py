@@ -1,5 +1,5 @@
-"""Small forwards of every kernel path for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck).  W = 1 by default (the sanitizer serialises kernels, which would stall a cross-rank
+"""Small forwards and backwards of every kernel path for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck).  W = 1 by default (the sanitizer serialises kernels, which would stall a cross-rank
 receive wait); --W 2 for memcheck of the loopback protocol.  Each output is checked against the
 oracle, so a sanitizer-induced difference would also show."""
 import argparse
@@ -44,6 +44,24 @@ for seed, (opts, pooling) in enumerate(cases):
         send = torch.zeros((p.B, p.T[r], p.D), device=dev)
         h.pool_local(idx[r], off[r], send)
     torch.cuda.synchronize()
+    # the backward (f3): sort plan, fused exchange + reduce + SGD (pass 1), cross-chunk fold
+    # (pass 2), twice (staging parity); integer gradients -> the oracle's tables bitwise
+    rng = np.random.default_rng(seed)
+    grads = [rng.integers(-4, 4, (p.b(s_), p.G * p.D)).astype(np.float32) for s_ in range(p.W)]
+    kw = {"pooling": oracle.MEAN} if pooling == "mean" else {}
+    if w is not None:
+        kw["weights"] = [np.ones(i.size, np.float32) for i in p.indices]
+    want = [t.copy() for t in p.tables]
+    for _ in range(2):
+        g.backward(idx, off, [torch.from_numpy(x).to(dev) for x in grads], 0.5, weights=w)
+        want = oracle.backward_sgd(p.part, p.D, p.B, p.T, want, p.indices, p.offsets, grads, 0.5,
+                                   **kw)
+    got = [t.cpu().numpy() for r in range(p.W) for t in g.handles[r]._tables]
+    for a_, b_ in zip(got, want):
+        if pooling == "mean":   # fl(g / L) is inexact: the summation order shows (R#31)
+            assert np.allclose(a_, b_, rtol=1e-6, atol=1e-5), ("backward", opts, pooling)
+        else:
+            assert np.array_equal(a_, b_), ("backward", opts, pooling)
     g.destroy()
     n += 1
-print(f"sanitize_smoke: {n} cases OK (W={args.W})")
+print(f"sanitize_smoke: {n} cases OK (W={args.W}), forward + backward")
