@@ -126,6 +126,17 @@ __device__ __forceinline__ unsigned long long lb_word(unsigned stamp, unsigned f
          count;
 }
 
+// Per-CTA timeline of a radix pass (the "trace" option): events 30 start, 31 tile loaded,
+// 32 ranked, 33 look-back done, 34 scattered; payload = tile.  Thread 0 only.
+__device__ __forceinline__ void ptrace(const PassParams& P, unsigned event, unsigned payload) {
+  if (P.trace == nullptr || threadIdx.x != 0) return;
+  const unsigned long long i = atomicAdd(P.trace, 1ull);
+  if ((long long)i >= P.trace_cap) return;
+  P.trace[2 + 2 * i] = ((unsigned long long)blockIdx.x << 40) |
+                       ((unsigned long long)event << 32) | payload;
+  P.trace[3 + 2 * i] = globaltimer();
+}
+
 // One stable LSD radix pass.  Tile = 4096 keys; warp w owns keys [w*512, (w+1)*512) of the
 // tile, item i of lane l at w*512 + i*32 + l (warp-striped, so "item, then lane" is position
 // order and the ranking below is stable).
@@ -143,6 +154,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   if (tid == 0) s_tile = atomicAdd(P.tile_ctr, 1u);
   __syncthreads();
   const long long tile = s_tile;
+  ptrace(P, 30, (unsigned)tile);
   const long long base = tile * kSortTile + (long long)w * (32 * kSortItems);
   const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -158,6 +170,12 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     bag[i] = valid ? P.bags_in[pos] : 0;
     if (WEIGHTS) wt[i] = valid ? P.wts_in[pos] : 0.f;
   }
+  if (P.trace) {                       // (tracing only: wait for the loads to time them)
+    unsigned x = 0;
+    for (int i = 0; i < kSortItems; ++i) x ^= key[i];
+    if (x == 0xdeadbeefu) s_tile = x;
+    ptrace(P, 31, (unsigned)tile);
+  }
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
@@ -170,6 +188,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     __syncwarp();
   }
   __syncthreads();
+  ptrace(P, 32, (unsigned)tile);
   // thread d: exclusive offsets of digit d per warp, the tile's count, the global base
   const unsigned d = tid;
   unsigned run = 0;
@@ -217,6 +236,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   }
   s_gofs[d] = gbase + excl;
   __syncthreads();
+  ptrace(P, 33, (unsigned)tile);
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
@@ -227,6 +247,10 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
       P.bags_out[out] = bag[i];
       if (WEIGHTS) P.wts_out[out] = wt[i];
     }
+  }
+  if (P.trace) {
+    __syncthreads();
+    ptrace(P, 34, (unsigned)tile);
   }
 }
 

@@ -185,6 +185,8 @@ struct PassParams {
   long long n;
   int shift;
   unsigned stamp;              // plan number (30 bits): stale look-back words are ignored
+  unsigned long long* trace;   // optional %globaltimer event log (the "trace" option)
+  long long trace_cap;
 };
 
 // The fused backward (exchange + reduce + update) and the unfused reduce share one kernel.

@@ -1101,6 +1101,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.n = n;
     q.shift = 8 * p;
     q.stamp = h->plan_no;
+    q.trace = h->d_trace;
+    q.trace_cap = h->trace_cap;
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);

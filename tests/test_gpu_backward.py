@@ -307,6 +307,26 @@ def test_rank_without_tables_and_uneven_tables():
     run.destroy()
 
 
+def test_backward_plan_validate_mode_rejects_bad_indices():
+    """validate=1: an out-of-range index or malformed offsets fail the plan with EINDEX
+    before any sort work is enqueued."""
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    from paper_2305_06942_b200.emb_a2a import EmbA2AError
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0), {"validate": 1})
+    t = torch.zeros(10, 8, device=dev())
+    h.register_tables([t], 4)
+    idx = torch.tensor([1, 2, 10, 3], dtype=torch.int32, device=dev())      # 10 >= rows
+    off = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int32, device=dev())
+    with pytest.raises(EmbA2AError) as e:
+        h.backward_plan(idx, off)
+    assert e.value.status == 8   # EMB_A2A_EINDEX
+    bad_off = torch.tensor([0, 3, 2, 3, 4], dtype=torch.int32, device=dev())  # decreasing
+    with pytest.raises(EmbA2AError) as e:
+        h.backward_plan(torch.tensor([1, 2, 3, 4], dtype=torch.int32, device=dev()), bad_off)
+    assert e.value.status == 8
+    h.destroy()
+
+
 def test_backward_rejects_half_tables_and_missing_plan():
     from paper_2305_06942_b200 import EmbA2A, LocalGroup
     from paper_2305_06942_b200.emb_a2a import EmbA2AError
