@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   for (int i = tid; i < NW * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
   pdl_wait();
   if (tid == 0) s_tile = atomicAdd(P.tile_ctr, 1u);
+  const unsigned hval = P.hist[tid];   // this pass's count of digit tid (for the global base)
   __syncthreads();
   const long long tile = s_tile;
   ptrace(P, 30, (unsigned)tile);
@@ -198,7 +199,6 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     s_cnt[ww][d] = run;
     run += c;
   }
-  const unsigned gbase = block_excl_scan256(P.hist[d], s_warp);
   unsigned long long* my = P.status + tile * 256 + d;
   unsigned excl = 0;
   if (tile == 0) {
@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     }
     st_relaxed_gpu(my, lb_word(P.stamp, 2, excl + run));
   }
+  // the digit's global base: exclusive scan of the pass histogram (after the look-back, so the
+  // tile's aggregate is published as early as possible)
+  const unsigned gbase = block_excl_scan256(hval, s_warp);
   s_gofs[d] = gbase + excl;
   __syncthreads();
   ptrace(P, 33, (unsigned)tile);
