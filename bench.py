@@ -564,15 +564,19 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
     plan_step(0)
     kern_ms = max_over_ranks(b2b_loop(lambda k: h.backward(grad, lr, stream), K, W)) / K
     un_ms = max_over_ranks(b2b_loop(unfused_step, K, W)) / K
-    # parity: fused vs unfused from the same tables on batch 0 (bitwise: same plan, same order)
-    snap = [t.clone() for t in h._tables]
+    # parity: fused vs unfused from the same tables on batch 0 (bitwise: same plan, same order);
+    # only the rows batch 0 touches can change (sparse SGD), so only those are snapshotted
+    idx0, off0 = mine[0]
+    rows = [torch.from_numpy(np.unique(idx0[off0[t * cfg.B]:off0[(t + 1) * cfg.B]]).astype(np.int64))
+            .to(dev) for t in range(T)]
+    snap = [tab[r].clone() for tab, r in zip(h._tables, rows)]
     fused_step(0)
-    after_f = [t.clone() for t in h._tables]
-    for t, s0 in zip(h._tables, snap):
-        t.copy_(s0)
+    after_f = [tab[r].clone() for tab, r in zip(h._tables, rows)]
+    for tab, r, s0 in zip(h._tables, rows, snap):
+        tab[r] = s0
     unfused_step(0)
     torch.cuda.synchronize()
-    same = all(bool(torch.equal(a, t)) for a, t in zip(after_f, h._tables))
+    same = all(bool(torch.equal(a, tab[r])) for a, tab, r in zip(after_f, h._tables, rows))
     # algorithmic bytes of the backward kernel (per launch, batch 0): gradient rows read once
     # (B * T_r * D * 4 at the owner + the pushed share), the sorted lookup list (key + bag,
     # 8 B per lookup), each distinct (table, row) read and written once
