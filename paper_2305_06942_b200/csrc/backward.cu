@@ -137,16 +137,21 @@ __device__ __forceinline__ void ptrace(const PassParams& P, unsigned event, unsi
   P.trace[3 + 2 * i] = globaltimer();
 }
 
-// One stable LSD radix pass.  Tile = 4096 keys; warp w owns keys [w*512, (w+1)*512) of the
-// tile, item i of lane l at w*512 + i*32 + l (warp-striped, so "item, then lane" is position
-// order and the ranking below is stable).
+// One stable LSD radix pass.  Tile = kSortTile keys; warp w owns keys [w*32*I, (w+1)*32*I) of
+// the tile (I = kSortItems), item i of lane l at w*32*I + i*32 + l (warp-striped, so "item,
+// then lane" is position order and the ranking below is stable).  The ranked tile is reordered
+// by digit in shared memory and written out one contiguous run per digit.
 template <bool WEIGHTS>
 __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassParams P) {
   constexpr int NW = kSortThreads / 32;
   __shared__ unsigned s_cnt[NW][256];   // running per-warp digit counts -> warp offsets in tile
   __shared__ unsigned s_gofs[256];
+  __shared__ unsigned s_tstart[256];    // first tile-local slot of each digit
   __shared__ unsigned s_warp[NW];
   __shared__ unsigned s_tile;
+  __shared__ unsigned s_key[kSortTile];  // the tile, reordered by digit (coalesced write-out)
+  __shared__ int s_bag[kSortTile];
+  __shared__ float s_wt[WEIGHTS ? kSortTile : 1];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   pdl_trigger();
   for (int i = tid; i < NW * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
@@ -238,18 +243,33 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   // tile's aggregate is published as early as possible)
   const unsigned gbase = block_excl_scan256(hval, s_warp);
   s_gofs[d] = gbase + excl;
+  __syncthreads();                       // s_warp is reused by the next scan
+  s_tstart[d] = block_excl_scan256(run, s_warp);
   __syncthreads();
   ptrace(P, 33, (unsigned)tile);
+  // reorder the tile by digit in shared memory, then write each digit's run of keys out
+  // contiguously (consecutive threads -> consecutive addresses within a run)
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
     if (pos < P.n) {
       const unsigned dd = (key[i] >> P.shift) & 255u;
-      const unsigned out = s_gofs[dd] + s_cnt[w][dd] + rank[i];
-      P.keys_out[out] = key[i];
-      P.bags_out[out] = bag[i];
-      if (WEIGHTS) P.wts_out[out] = wt[i];
+      const unsigned lp = s_tstart[dd] + s_cnt[w][dd] + rank[i];
+      s_key[lp] = key[i];
+      s_bag[lp] = bag[i];
+      if (WEIGHTS) s_wt[lp] = wt[i];
     }
+  }
+  __syncthreads();
+  const long long t0 = tile * kSortTile;
+  const int tn = (P.n - t0) < kSortTile ? (int)(P.n - t0) : kSortTile;
+  for (int i = tid; i < tn; i += kSortThreads) {
+    const unsigned k = s_key[i];
+    const unsigned dd = (k >> P.shift) & 255u;
+    const unsigned out = s_gofs[dd] + (unsigned)i - s_tstart[dd];
+    P.keys_out[out] = k;
+    P.bags_out[out] = s_bag[i];
+    if (WEIGHTS) P.wts_out[out] = s_wt[i];
   }
   if (P.trace) {
     __syncthreads();
