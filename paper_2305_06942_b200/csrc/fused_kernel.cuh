@@ -507,13 +507,25 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
       s_flag[i] = nullptr;
     }
   }
-  // Everything below reads inputs / counters / buffers a predecessor on the stream may write:
-  // wait for it (a no-op without a programmatic predecessor).
-  if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
+  // Programmatic dependent launch: everything that reads table rows, counters or buffers a
+  // predecessor on the stream may write waits for it (griddepcontrol.wait; a no-op without a
+  // programmatic predecessor).  The producer's first reads -- the first chunk's CSR offsets and
+  // the first stage's index copy -- touch only the caller's inputs, which no kernel of this
+  // library writes (and a caller kernel that does is not a programmatic predecessor: it has
+  // completed before this grid launched), so in the LSU mode they go ahead of the wait and
+  // overlap the predecessor's drain.
 
   if (warp == 0) {
     // ===================================================================== producer
+    bool waited = !P.pdl;
+    auto pdl_wait_once = [&]() {
+      if (!waited) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+    };
+    if (TMA) pdl_wait_once();            // the producer gathers table rows itself
     if (lane32 == 0) trace_ev(P, 0, 0);
     int u = 0;   // stage uses so far
     // wait until consumers released use v; for a remote slice, publish its bags (a7)
@@ -630,6 +642,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
           mbar_arrive(&full_bar[st]);
           cp_async_mbar_arrive(&full_bar[st]);
         }
+        pdl_wait_once();                 // before any recycle (counters) or a next stage
         if (lane32 == 0) trace_ev(P, 2, (unsigned)u);
         cb += n;
         ++u;
@@ -638,6 +651,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
       k = k2; s = s2; t = t2; i0 = i02; nb = nb2; o0 = p0; o1 = p1;
     }
     // end marker, then drain: every outstanding stage is consumed and published
+    pdl_wait_once();
     {
       const int st = u % NS;
       if (u >= NS) recycle(u - NS);
@@ -649,6 +663,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
     }
   } else {
     // ===================================================================== consumers
+    if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int ctid = tid - 32;
     const int lane = ctid % LPB;
     const int group = ctid / LPB;
