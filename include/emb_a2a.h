@@ -220,6 +220,12 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *   "pdl"          1 = programmatic dependent launch (default): the kernel's CTAs may start while
  *                  the previous kernel on the stream drains; all reads of inputs, counters and
  *                  buffers wait (griddepcontrol.wait) for that kernel to complete
+ *   "pdl_rows_early"  1 (default): with one rank (W = 1), a forward's table-row reads and stores
+ *                  skip the programmatic wait when this handle has launched no backward since its
+ *                  previous forward (the predecessor can then only be a forward, which never
+ *                  writes tables or this forward's receive buffer).  Set 0 if a
+ *                  kernel of your own that writes the tables and triggers programmatic launch
+ *                  (griddepcontrol.launch_dependents) can directly precede a forward on its stream
  *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
  *                  fewer lanes per bag keeps more bags in flight per warp
  *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)

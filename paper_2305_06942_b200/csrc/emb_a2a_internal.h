@@ -63,6 +63,7 @@ struct KParams {
   int payload_off;    // offset of the rows / indices inside a stage
   int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
   int pdl;            // programmatic dependent launch (overlap with the stream predecessor)
+  int rows_wait;      // consumers wait for the predecessor before reading table rows
   int flat_below;     // stages whose average bag length is below this use row-flattened pooling
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices

@@ -663,7 +663,10 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
     }
   } else {
     // ===================================================================== consumers
-    if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // table rows and receive-buffer stores: wait for the predecessor unless the host found it
+    // harmless (one rank, no backward of this handle since its previous forward; option
+    // "pdl_rows_early"); the counters are the producer's, and it always waits
+    if (P.pdl && P.rows_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int ctid = tid - 32;
     const int lane = ctid % LPB;
     const int group = ctid / LPB;

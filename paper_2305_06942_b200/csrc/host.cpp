@@ -83,7 +83,8 @@ struct emb_a2a {
   // options
   int64_t S = 32, order = 0, threads = 256, timeout_ms = 10000, validate = 0, unroll = 0;
   int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, tma = 0;
-  int64_t stage_kb = 32, vec = 0, pdl = 1, flat_below = 12;
+  int64_t stage_kb = 32, vec = 0, pdl = 1, flat_below = 12, rows_early = 1;
+  bool tables_dirty = true;              // a table writer may precede the next forward
   int64_t chunk = 32;
   int64_t trace_cap = 0;                 // records; 0 = tracing off
   unsigned long long* d_trace = nullptr;
@@ -327,6 +328,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.slice_cnt = h->d_slice_cnt;
   P.nstages = (int)h->stages;
   P.pdl = (int)h->pdl;
+  P.rows_wait = 1;
   P.flat_below = (int)h->flat_below;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
@@ -662,6 +664,7 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   h->bepoch = 0;
   h->planned = false;
   h->bwd_mode = -1;
+  h->tables_dirty = true;
   for (int w = 0; w < 2; ++w) {
     h->plan_fused[w] = LaunchPlan();
     h->plan_pool[w] = LaunchPlan();
@@ -702,6 +705,12 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
   h->epoch += 1;
   const float* w = num_indices > 0 ? weights : nullptr;
   KParams P = make_params(h, indices, offsets, w);
+  // consumers may gather rows before the predecessor completes only with one rank (with peers,
+  // an early store could land in a peer's receive buffer before that peer consumed it: the
+  // buffer-reuse argument needs this rank's previous forward complete first) and
+  // when no backward of this handle (the only table writer) ran since the previous forward
+  P.rows_wait = (h->W > 1 || h->tables_dirty || !h->rows_early) ? 1 : 0;
+  h->tables_dirty = false;
   LaunchPlan& pl = h->plan_fused[w ? 1 : 0];
   cudaError_t e = cudaSuccess;
   if (!pl.fn) {
@@ -972,6 +981,7 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
 }
 
 int run_backward(emb_a2a* h, BwdParams& P, cudaStream_t st) {
+  h->tables_dirty = true;   // the next forward's table reads wait for this kernel
   const int mode = P.wts ? 1 : (P.mean ? 2 : 0);
   if (h->bwd_mode != mode) {
     cudaError_t e = plan_backward(P, (int)h->bwd_threads, (int)h->bwd_share, &h->bwd_grid,
@@ -1238,6 +1248,8 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
       CUDA_TRY(h, cudaDeviceSynchronize());   // legacy-stream memset vs. non-blocking streams
       h->trace_cap = v;
     }
+  } else if (k == "pdl_rows_early") {
+    h->rows_early = v ? 1 : 0;
   } else if (k == "bwd_threads") {
     if (v < 32 || v > 256 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..256, x32");
     h->bwd_threads = v;
@@ -1274,6 +1286,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "flat_below") *v = h->flat_below;
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
+  else if (k == "pdl_rows_early") *v = h->rows_early;
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;

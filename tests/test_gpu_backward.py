@@ -260,6 +260,36 @@ def test_training_steps_forward_backward_interleaved():
     run.destroy()
 
 
+def test_single_rank_forward_backward_forward_no_sync():
+    """W=1, one stream, no host sync: forward, forward (its table reads may overlap the previous
+    forward's drain), plan + backward (writes the tables), forward (must see the update: its
+    reads wait for the backward), forward.  Every output equals the oracle on the tables of its
+    time, bitwise (exact-int)."""
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    p = random_problem(5700, W=1, value_mode=1, max_B=128, max_D=64)
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    tabs = [torch.from_numpy(np.ascontiguousarray(t)).to(dev()) for t in p.tables]
+    h.register_tables(tabs, p.B)
+    idx = torch.from_numpy(p.indices[0]).to(dev())
+    off = torch.from_numpy(p.offsets[0]).to(dev())
+    grads = grads_for(p, 3, 1)
+    g = torch.from_numpy(grads[0]).to(dev())
+    outs = []
+    for k in range(2):
+        outs.append(h.forward(idx, off).clone())
+    h.backward_plan(idx, off)
+    h.backward(g, -1.0)
+    for k in range(2):
+        outs.append(h.forward(idx, off).clone())
+    torch.cuda.synchronize()
+    ref0 = oracle.emb_a2a(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets)[0]
+    new = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, -1.0)
+    ref1 = oracle.emb_a2a(p.part, p.D, p.B, p.T, new, p.indices, p.offsets)[0]
+    for k, o in enumerate(outs):
+        np.testing.assert_array_equal(o.cpu().numpy(), ref0 if k < 2 else ref1)
+    h.destroy()
+
+
 def test_empty_plan_and_empty_blocks():
     """No lookups at all on one rank, a rank with an empty batch block, all-empty bags."""
     D, B = 8, 6
