@@ -241,6 +241,9 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  its indices from global memory
  *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
  *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
+ *   "sort_mode"    backward plan's radix passes: 0 auto (default: one kernel per pass with
+ *                  look-back while the tiles fit one wave, else three kernels per pass,
+ *                  reduce-then-scan), 1 always one kernel, 2 always three (results identical)
  *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 256] (default 128)
  *   "bwd_share"    divide the backward's persistent grid by this (default 1): W virtual ranks on
  *                  one GPU must all be resident at once (loopback sets it to W)

@@ -13,9 +13,10 @@
 // Kernels:
 //   bwd_keygen_kernel    key_k = t << rbits | idx_k, payload bag_k (+ w_k); digit histograms of
 //                        every radix pass at once (upfront histogram)
-//   bwd_onesweep_kernel  one stable LSD radix pass (8-bit digit): warp-level ranking with
-//                        match.any, per-digit decoupled look-back across tiles (tiles taken in
-//                        ticket order, so every look-back target is already running)
+//   bwd_upsweep_kernel / bwd_scan_kernel / bwd_downsweep_kernel
+//                        one stable LSD radix pass (8-bit digit), reduce-then-scan: tile digit
+//                        counts, a per-digit scan over tiles, then warp-level ranking with
+//                        match.any and a digit-ordered, contiguous write-out of each tile
 //   bwd_kernel           (fused) each CTA first pushes its share of this rank's gradient rows
 //                        straight into the owners' staging buffers over NVLink (zero-copy, the
 //                        reverse of P:165) and signals the owner's per-source counter with
@@ -119,15 +120,8 @@ __device__ __forceinline__ unsigned block_excl_scan256(unsigned v, unsigned* s_w
   return base + x - v;
 }
 
-// Look-back words: [63:34] stamp | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] count
-__device__ __forceinline__ unsigned long long lb_word(unsigned stamp, unsigned flag,
-                                                      unsigned count) {
-  return ((unsigned long long)(stamp & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) |
-         count;
-}
-
 // Per-CTA timeline of a radix pass (the "trace" option): events 30 start, 31 tile loaded,
-// 32 ranked, 33 look-back done, 34 scattered; payload = tile.  Thread 0 only.
+// 32 ranked, 33 offsets known, 34 scattered; payload = tile.  Thread 0 only.
 __device__ __forceinline__ void ptrace(const PassParams& P, unsigned event, unsigned payload) {
   if (P.trace == nullptr || threadIdx.x != 0) return;
   const unsigned long long i = atomicAdd(P.trace, 1ull);
@@ -137,7 +131,15 @@ __device__ __forceinline__ void ptrace(const PassParams& P, unsigned event, unsi
   P.trace[3 + 2 * i] = globaltimer();
 }
 
-// One stable LSD radix pass.  Tile = kSortTile keys; warp w owns keys [w*32*I, (w+1)*32*I) of
+// Look-back words: [63:34] stamp | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] count
+__device__ __forceinline__ unsigned long long lb_word(unsigned stamp, unsigned flag,
+                                                      unsigned count) {
+  return ((unsigned long long)(stamp & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) |
+         count;
+}
+
+// One stable LSD radix pass in ONE kernel (onesweep; used when all tiles fit in one wave, so the
+// look-back chains are short and the launch count matters more).  Tile = kSortTile keys; warp w owns keys [w*32*I, (w+1)*32*I) of
 // the tile (I = kSortItems), item i of lane l at w*32*I + i*32 + l (warp-striped, so "item,
 // then lane" is position order and the ranking below is stable).  The ranked tile is reordered
 // by digit in shared memory and written out one contiguous run per digit.
@@ -244,6 +246,155 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   const unsigned gbase = block_excl_scan256(hval, s_warp);
   s_gofs[d] = gbase + excl;
   __syncthreads();                       // s_warp is reused by the next scan
+  s_tstart[d] = block_excl_scan256(run, s_warp);
+  __syncthreads();
+  ptrace(P, 33, (unsigned)tile);
+  // reorder the tile by digit in shared memory, then write each digit's run of keys out
+  // contiguously (consecutive threads -> consecutive addresses within a run)
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const long long pos = base + i * 32 + lane;
+    if (pos < P.n) {
+      const unsigned dd = (key[i] >> P.shift) & 255u;
+      const unsigned lp = s_tstart[dd] + s_cnt[w][dd] + rank[i];
+      s_key[lp] = key[i];
+      s_bag[lp] = bag[i];
+      if (WEIGHTS) s_wt[lp] = wt[i];
+    }
+  }
+  __syncthreads();
+  const long long t0 = tile * kSortTile;
+  const int tn = (P.n - t0) < kSortTile ? (int)(P.n - t0) : kSortTile;
+  for (int i = tid; i < tn; i += kSortThreads) {
+    const unsigned k = s_key[i];
+    const unsigned dd = (k >> P.shift) & 255u;
+    const unsigned out = s_gofs[dd] + (unsigned)i - s_tstart[dd];
+    P.keys_out[out] = k;
+    P.bags_out[out] = s_bag[i];
+    if (WEIGHTS) P.wts_out[out] = s_wt[i];
+  }
+  if (P.trace) {
+    __syncthreads();
+    ptrace(P, 34, (unsigned)tile);
+  }
+}
+
+// One stable LSD radix pass = three kernels (reduce-then-scan: no look-back chains, so tiles of
+// one wave do not wait on each other).
+//   upsweep:   each tile's digit counts -> cnt[digit][tile]
+//   scan:      one CTA per digit: cnt[d][t] <- (keys with a smaller digit) + sum_{t' < t} cnt[d][t']
+//              = the global position of tile t's first key with digit d (digit-major order)
+//   downsweep: rank each key within its tile (stable), reorder the tile by digit in shared
+//              memory, write each digit's run to its global position (contiguous writes)
+__global__ void __launch_bounds__(kSortThreads) bwd_upsweep_kernel(const PassParams P) {
+  __shared__ unsigned h[256];
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  h[tid] = 0u;
+  pdl_wait();
+  __syncthreads();
+  const long long t0 = (long long)blockIdx.x * kSortTile;
+  for (int i = tid; i < kSortTile; i += kSortThreads) {
+    const long long pos = t0 + i;
+    if (pos < P.n) atomicAdd(&h[(P.keys_in[pos] >> P.shift) & 255u], 1u);
+  }
+  __syncthreads();
+  P.cnt[(long long)tid * P.ntiles + blockIdx.x] = h[tid];
+}
+
+__global__ void __launch_bounds__(256) bwd_scan_kernel(const PassParams P) {
+  __shared__ unsigned s_warp[8];
+  __shared__ unsigned s_carry;
+  const int tid = threadIdx.x, d = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  // keys with a digit below d (the pass histogram from keygen)
+  const unsigned below = block_excl_scan256(P.hist[tid], s_warp);
+  if (tid == d) s_carry = below;
+  __syncthreads();
+  unsigned* row = P.cnt + (long long)d * P.ntiles;
+  constexpr int K = 4;                       // consecutive tiles per thread
+  for (long long t0 = 0; t0 < P.ntiles; t0 += 256 * K) {
+    unsigned x[K], sum = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const long long t = t0 + (long long)tid * K + k;
+      x[k] = t < P.ntiles ? row[t] : 0u;
+      sum += x[k];
+    }
+    const unsigned carry = s_carry;
+    __syncthreads();                         // s_warp / s_carry reuse below
+    const unsigned ex = block_excl_scan256(sum, s_warp);
+    unsigned run = carry + ex;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const long long t = t0 + (long long)tid * K + k;
+      if (t < P.ntiles) row[t] = run;
+      run += x[k];
+    }
+    if (tid == 255) s_carry = run;           // = carry + this block's total
+    __syncthreads();
+  }
+}
+
+// Warp-striped tile: warp w owns keys [w*32*I, (w+1)*32*I) of the tile (I = kSortItems), item i
+// of lane l at w*32*I + i*32 + l, so "item, then lane" is position order and the ranking is
+// stable.
+template <bool WEIGHTS>
+__global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassParams P) {
+  constexpr int NW = kSortThreads / 32;
+  __shared__ unsigned s_cnt[NW][256];   // running per-warp digit counts -> warp offsets in tile
+  __shared__ unsigned s_gofs[256];
+  __shared__ unsigned s_tstart[256];    // first tile-local slot of each digit
+  __shared__ unsigned s_warp[NW];
+  __shared__ unsigned s_key[kSortTile];  // the tile, reordered by digit (contiguous write-out)
+  __shared__ int s_bag[kSortTile];
+  __shared__ float s_wt[WEIGHTS ? kSortTile : 1];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long tile = blockIdx.x;
+  pdl_trigger();
+  for (int i = tid; i < NW * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
+  pdl_wait();
+  __syncthreads();
+  ptrace(P, 30, (unsigned)tile);
+  const long long base = tile * kSortTile + (long long)w * (32 * kSortItems);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned key[kSortItems];
+  int bag[kSortItems];
+  float wt[kSortItems];
+  unsigned short rank[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const long long pos = base + i * 32 + lane;
+    const bool valid = pos < P.n;
+    key[i] = valid ? P.keys_in[pos] : 0u;
+    bag[i] = valid ? P.bags_in[pos] : 0;
+    if (WEIGHTS) wt[i] = valid ? P.wts_in[pos] : 0.f;
+  }
+  const unsigned d = tid;
+  const unsigned gofs = P.cnt[(long long)d * P.ntiles + tile];   // scanned by bwd_scan_kernel
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const long long pos = base + i * 32 + lane;
+    const unsigned dg = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
+    const unsigned peers = __match_any_sync(kFull, dg);
+    const unsigned c = dg < 256u ? s_cnt[w][dg] : 0u;
+    rank[i] = (unsigned short)(c + __popc(peers & lt_mask));
+    __syncwarp();
+    if (dg < 256u && lane == __ffs(peers) - 1) s_cnt[w][dg] = c + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  ptrace(P, 32, (unsigned)tile);
+  // thread d: exclusive offsets of digit d per warp, the tile's count of d
+  unsigned run = 0;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) {
+    const unsigned c = s_cnt[ww][d];
+    s_cnt[ww][d] = run;
+    run += c;
+  }
+  s_gofs[d] = gofs;
   s_tstart[d] = block_excl_scan256(run, s_warp);
   __syncthreads();
   ptrace(P, 33, (unsigned)tile);
@@ -749,19 +900,37 @@ size_t bwd_smem(const BwdParams& P, int threads) {
 }  // namespace
 
 cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int npasses,
-                             long long ntiles, int grid_keygen, cudaStream_t st) {
+                             long long ntiles, int grid_keygen, int mode, cudaStream_t st) {
   if (S.TB > 0) {
     if (S.weights) bwd_keygen_kernel<true><<<grid_keygen, 256, 0, st>>>(S);
     else bwd_keygen_kernel<false><<<grid_keygen, 256, 0, st>>>(S);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  // one wave of tiles: onesweep (1 kernel per pass, short look-back); more: reduce-then-scan
+  // (3 kernels per pass, no look-back chains across the tiles of a wave)
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool one_wave = mode == 1 || (mode == 0 && ntiles <= 3LL * sms);
   for (int p = 0; p < npasses; ++p) {
     PassParams pp = passes[p];
     void* args[] = {&pp};
-    const void* fn = passes[p].wts_in ? reinterpret_cast<const void*>(bwd_onesweep_kernel<true>)
-                                      : reinterpret_cast<const void*>(bwd_onesweep_kernel<false>);
-    cudaError_t e = launch_pdl(fn, (unsigned)ntiles, kSortThreads, 0, st, args);
+    if (one_wave) {
+      const void* fn = passes[p].wts_in
+                           ? reinterpret_cast<const void*>(bwd_onesweep_kernel<true>)
+                           : reinterpret_cast<const void*>(bwd_onesweep_kernel<false>);
+      cudaError_t e = launch_pdl(fn, (unsigned)ntiles, kSortThreads, 0, st, args);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
+    cudaError_t e = launch_pdl(reinterpret_cast<const void*>(bwd_upsweep_kernel),
+                               (unsigned)ntiles, kSortThreads, 0, st, args);
+    if (e == cudaSuccess)
+      e = launch_pdl(reinterpret_cast<const void*>(bwd_scan_kernel), 256, 256, 0, st, args);
+    const void* fn = passes[p].wts_in ? reinterpret_cast<const void*>(bwd_downsweep_kernel<true>)
+                                      : reinterpret_cast<const void*>(bwd_downsweep_kernel<false>);
+    if (e == cudaSuccess) e = launch_pdl(fn, (unsigned)ntiles, kSortThreads, 0, st, args);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -181,8 +181,10 @@ struct PassParams {
   const float* wts_in;         // NULL = no weight payload
   float* wts_out;
   const unsigned* hist;        // this pass's 256 digit counts
-  unsigned long long* status;  // [ntiles][256] look-back words of this pass
-  unsigned* tile_ctr;          // this pass's tile ticket (zeroed before keygen)
+  unsigned* cnt;               // [256][ntiles] tile digit counts -> global digit offsets
+  unsigned long long* status;  // onesweep: [ntiles][256] look-back words of this pass
+  unsigned* tile_ctr;          // onesweep: this pass's tile ticket (zeroed before keygen)
+  long long ntiles;
   long long n;
   int shift;
   unsigned stamp;              // plan number (30 bits): stale look-back words are ignored
@@ -221,8 +223,10 @@ struct BwdParams {
   int tofs[kMaxW];
 };
 
+// mode: 0 auto (onesweep while the tiles fit one wave, else reduce-then-scan), 1 onesweep,
+// 2 reduce-then-scan
 cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int npasses,
-                             long long ntiles, int grid_keygen, cudaStream_t st);
+                             long long ntiles, int grid_keygen, int mode, cudaStream_t st);
 cudaError_t plan_backward(const BwdParams& P, int threads, int share, unsigned* grid,
                           size_t* smem);
 cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size_t smem,

@@ -131,7 +131,7 @@ struct emb_a2a {
   int64_t kernel_launches = 0;
 
   // backward (f3)
-  int64_t bwd_threads = 128, bwd_share = 1;
+  int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0;
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
   unsigned long long* bflags = nullptr;  // own backward arrival counters
@@ -141,7 +141,9 @@ struct emb_a2a {
   float* d_wts[2] = {nullptr, nullptr};
   size_t plan_cap = 0, wts_cap = 0;
   unsigned* d_hist = nullptr;            // [kMaxPasses][256] + kMaxPasses tile tickets
-  unsigned long long* d_status = nullptr;
+  unsigned* d_cnt = nullptr;             // radix pass: [256][ntiles] tile digit counts
+  size_t cnt_cap = 0;
+  unsigned long long* d_status = nullptr;  // onesweep look-back words
   size_t status_cap = 0;
   float* d_scratch = nullptr;
   unsigned char* d_info = nullptr;       // per-chunk crossing-run flags (backward pass 2)
@@ -228,11 +230,14 @@ void release_registration(emb_a2a* h) {
   }
   h->plan_cap = h->wts_cap = 0;
   if (h->d_hist) cudaFree(h->d_hist);
+  if (h->d_cnt) cudaFree(h->d_cnt);
   if (h->d_status) cudaFree(h->d_status);
+  h->d_status = nullptr;
+  h->cnt_cap = 0;
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->d_info) cudaFree(h->d_info);
   h->d_hist = nullptr;
-  h->d_status = nullptr;
+  h->d_cnt = nullptr;
   h->d_scratch = nullptr;
   h->d_info = nullptr;
   h->status_cap = h->chunk_cap = 0;
@@ -1060,7 +1065,13 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     if ((rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses + 1))) return rc;
     CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (kMaxPasses * 256 + kMaxPasses + 1) * 4, st));
   }
-  const size_t nstatus = (size_t)passes * ntiles * 256;
+  const size_t ncnt = (size_t)ntiles * 256;      // tile digit counts of one pass
+  if (ncnt > h->cnt_cap) {
+    const size_t scap = ncnt + ncnt / 4 + 256;
+    if ((rc = grow(h, &h->d_cnt, scap))) return rc;
+    h->cnt_cap = scap;
+  }
+  const size_t nstatus = (size_t)passes * ntiles * 256;   // onesweep look-back words
   if (nstatus > h->status_cap) {
     const size_t scap = nstatus + nstatus / 4 + 4 * 256;
     if ((rc = grow(h, &h->d_status, scap))) return rc;
@@ -1106,8 +1117,10 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.wts_in = wtd ? h->d_wts[p & 1] : nullptr;
     q.wts_out = wtd ? h->d_wts[(p + 1) & 1] : nullptr;
     q.hist = h->d_hist + p * 256;
+    q.cnt = h->d_cnt;
     q.status = h->d_status + (size_t)p * ntiles * 256;
     q.tile_ctr = h->d_hist + kMaxPasses * 256 + p;
+    q.ntiles = ntiles;
     q.n = n;
     q.shift = 8 * p;
     q.stamp = h->plan_no;
@@ -1119,7 +1132,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long TB = (long long)h->T * h->B;
   const long long gk = std::min<long long>((TB + 63) / 64, (long long)sms * 8);   // 8 bags/warp
-  cudaError_t e = launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1), st);
+  cudaError_t e = launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1),
+                                   (int)h->sort_mode, st);
   if (e != cudaSuccess) {
     h->planned = false;
     return fail(h, EMB_A2A_ECUDA, "backward plan launch: %s", cudaGetErrorString(e));
@@ -1250,6 +1264,9 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     }
   } else if (k == "pdl_rows_early") {
     h->rows_early = v ? 1 : 0;
+  } else if (k == "sort_mode") {
+    if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2}");
+    h->sort_mode = v;
   } else if (k == "bwd_threads") {
     if (v < 32 || v > 256 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..256, x32");
     h->bwd_threads = v;
@@ -1287,6 +1304,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
   else if (k == "pdl_rows_early") *v = h->rows_early;
+  else if (k == "sort_mode") *v = h->sort_mode;
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;

@@ -116,6 +116,47 @@ def test_tiny_config_backward_exact():
 
 # ------------------------------------------------------------------------------- fp32 mode
 
+@pytest.mark.parametrize("sort_mode", [1, 2])
+@pytest.mark.parametrize("seed", range(3))
+def test_both_radix_schemes_exact(seed, sort_mode):
+    """The plan's radix passes as one kernel with look-back (1) or as upsweep / scan /
+    downsweep (2): same sorted plan, so the same tables bitwise (exact-int), incl. weights."""
+    p = random_problem(5800 + seed, value_mode=1, ragged=seed == 1, max_B=128, max_D=64)
+    grads = grads_for(p, seed, 1)
+    weights = None
+    kw = {}
+    if seed == 2:
+        cfg = synth.config_for("tiny")
+        weights = [np.ones(i.size, np.float32) * 2 for i in p.indices]
+        kw["weights"] = weights
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 1.0, **kw)
+    run = Run(p, opts={"sort_mode": sort_mode})
+    run.backward(grads, 1.0, weights=weights)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+def test_reduce_then_scan_many_tiles():
+    """More than a wave of radix tiles (auto mode switches to reduce-then-scan): ~1.2 M lookups
+    over 2 small tables, exact-int."""
+    rng = np.random.default_rng(59)
+    D, B = 8, 8192
+    R = [48, 33]
+    tables = [rng.integers(-8, 8, (r, D)).astype(np.float32) for r in R]
+    bags = [[list(rng.integers(0, R[t], rng.integers(50, 100))) for _ in range(B)] for t in range(2)]
+    i, o = csr_from_bags(bags)
+    assert i.size > 3 * 148 * 2048
+    p = Problem(1, [2], D, B, np.array([0, B]), tables, [i], [o])
+    grads = grads_for(p, 9, 1)
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 0.5)
+    run = Run(p)
+    run.backward(grads, 0.5)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_backward_fp32_within_rounding_bound(seed):
     p = random_problem(5100 + seed, value_mode=0, ragged=seed % 3 == 1, max_B=128, max_D=128)
