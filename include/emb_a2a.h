@@ -225,7 +225,10 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  previous forward (the predecessor can then only be a forward, which never
  *                  writes tables or this forward's receive buffer).  Set 0 if a
  *                  kernel of your own that writes the tables and triggers programmatic launch
- *                  (griddepcontrol.launch_dependents) can directly precede a forward on its stream
+ *                  (griddepcontrol.launch_dependents) can directly precede a forward on its stream.
+ *                  With peers, the first stage for a peer is held until that peer has provably
+ *                  consumed the buffer half it overwrites; off when a peer shares this GPU (its
+ *                  CTAs could need the slots), 2 = on even then (tests, small grids)
  *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
  *                  fewer lanes per bag keeps more bags in flight per warp
  *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)

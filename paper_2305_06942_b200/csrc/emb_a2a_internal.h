@@ -64,6 +64,7 @@ struct KParams {
   int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
   int pdl;            // programmatic dependent launch (overlap with the stream predecessor)
   int rows_wait;      // consumers wait for the predecessor before reading table rows
+  int pdl_trigger;    // trigger the dependent launch at CTA start (else only by exiting)
   int flat_below;     // stages whose average bag length is below this use row-flattened pooling
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices

@@ -495,7 +495,9 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
   }
   // Programmatic dependent launch: let the next kernel on the stream start its CTAs (launch ramp,
   // prologue) as ours retire; it waits at griddepcontrol.wait for us to finish.
-  if (P.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // (Not when a peer shares this GPU: a rank running ahead would park the waiting CTAs of its
+  // next forwards on SM slots a slower peer's forward needs; exiting triggers it then.)
+  if (P.pdl && P.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = tid; i < P.T && i < kMaxSmemTables; i += blockDim.x)
     s_tab[i] = reinterpret_cast<const uint4*>(P.tables[i]);
   for (int i = tid; i < P.W; i += blockDim.x) {
@@ -637,6 +639,32 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
               const float* wg = P.weights + base;
               const unsigned sw = si + 4u * (unsigned)P.payload_cap;
               for (int q = lane32; q < cnt; q += 32) cp_async4(sw + 4u * (unsigned)q, wg + q);
+            }
+          }
+          // This stage is published before the predecessor is known complete (only the first
+          // one is).  If its consumers do not wait either (rows_wait == 0) and it goes to a
+          // peer, the peer must be done with the buffer half it will overwrite -- the output of
+          // our epoch - 2, which the peer consumed before starting its forward epoch - 1.  The
+          // peer's epoch-(epoch-1) slices for us having all arrived proves it started it
+          // (DESIGN.md §5); a peer that sends us nothing gives no such proof: wait instead.
+          if (FUSED && !waited && !P.rows_wait && s != P.r) {
+            const long long nin = P.peers->n_in[s];
+            if (nin == 0) {
+              pdl_wait_once();
+            } else {
+              if (lane32 == 0) {
+                const unsigned long long target = (P.epoch - 1ull) * (unsigned long long)nin;
+                const unsigned long long* f = P.flags_in + (size_t)s * kFlagStride;
+                const unsigned long long t0 = globaltimer();
+                while (ld_acquire_sys(f) < target) {
+                  if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
+                    atomicExch(P.err, 0x100 | s);
+                    break;
+                  }
+                  __nanosleep(64);
+                }
+              }
+              __syncwarp();
             }
           }
           mbar_arrive(&full_bar[st]);

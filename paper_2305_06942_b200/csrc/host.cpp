@@ -40,6 +40,7 @@ struct Handles {        // phase-2 all-gather record (symmetric region)
   uint64_t raw_ptr;
   uint64_t region_bytes;
   cudaIpcMemHandle_t ipc;
+  char bus_id[32];      // PCI bus id of the device: peers on the same physical GPU co-reside
 };
 
 uint64_t host_id() {
@@ -85,6 +86,7 @@ struct emb_a2a {
   int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, tma = 0;
   int64_t stage_kb = 32, vec = 0, pdl = 1, flat_below = 12, rows_early = 1;
   bool tables_dirty = true;              // a table writer may precede the next forward
+  bool shared_gpu = false;               // some peer runs on this same GPU
   int64_t chunk = 32;
   int64_t trace_cap = 0;                 // records; 0 = tracing off
   unsigned long long* d_trace = nullptr;
@@ -334,6 +336,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.nstages = (int)h->stages;
   P.pdl = (int)h->pdl;
   P.rows_wait = 1;
+  P.pdl_trigger = (h->W > 1 && h->shared_gpu && h->rows_early != 2) ? 0 : 1;
   P.flat_below = (int)h->flat_below;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
@@ -591,6 +594,7 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   mine.magic = kMagic;
   mine.pid = (int32_t)getpid();
   mine.device = h->dev;
+  cudaDeviceGetPCIBusId(mine.bus_id, sizeof(mine.bus_id), h->dev);
   mine.host_id = host_id();
   mine.raw_ptr = (uint64_t)(uintptr_t)h->region;
   mine.region_bytes = h->region_bytes;
@@ -601,9 +605,13 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
 
   // ---- map every peer (roc_shmem_ptr gives the peer's virtual address)
   memset(&h->host_peers, 0, sizeof(DevPeers));
+  h->shared_gpu = false;
   for (int q = 0; q < h->W; ++q) {
     char* base = nullptr;
     const Handles& o = hs[q];
+    if (q != h->rank && o.host_id == mine.host_id &&
+        strncmp(o.bus_id, mine.bus_id, sizeof(mine.bus_id)) == 0)
+      h->shared_gpu = true;   // a peer on this very GPU (virtual ranks / shared-GPU test mode)
     if (q == h->rank) {
       base = h->region;
     } else if (o.pid == mine.pid && o.host_id == mine.host_id) {
@@ -710,11 +718,16 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
   h->epoch += 1;
   const float* w = num_indices > 0 ? weights : nullptr;
   KParams P = make_params(h, indices, offsets, w);
-  // consumers may gather rows before the predecessor completes only with one rank (with peers,
-  // an early store could land in a peer's receive buffer before that peer consumed it: the
-  // buffer-reuse argument needs this rank's previous forward complete first) and
-  // when no backward of this handle (the only table writer) ran since the previous forward
-  P.rows_wait = (h->W > 1 || h->tables_dirty || !h->rows_early) ? 1 : 0;
+  // consumers may gather rows and store before the predecessor completes when no backward of
+  // this handle (the only table writer) ran since the previous forward; with peers, the
+  // producer holds back the one stage it publishes before its own wait until the destination
+  // peer has provably consumed the buffer half (fused_kernel.cuh)
+  // (not when a peer shares this GPU: a stage held back for that peer would keep CTAs resident
+  // that the peer's own forward may need)
+  // ("pdl_rows_early" = 2 forces it on a shared GPU too: tests, with grids small enough to
+  // co-reside)
+  P.rows_wait = (h->tables_dirty || !h->rows_early ||
+                 (h->W > 1 && h->shared_gpu && h->rows_early != 2)) ? 1 : 0;
   h->tables_dirty = false;
   LaunchPlan& pl = h->plan_fused[w ? 1 : 0];
   cudaError_t e = cudaSuccess;
@@ -1263,7 +1276,8 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
       h->trace_cap = v;
     }
   } else if (k == "pdl_rows_early") {
-    h->rows_early = v ? 1 : 0;
+    if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "pdl_rows_early in {0, 1, 2}");
+    h->rows_early = v;
   } else if (k == "sort_mode") {
     if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2}");
     h->sort_mode = v;

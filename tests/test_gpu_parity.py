@@ -325,6 +325,57 @@ def test_forward_host_end_to_end():
     g.destroy()
 
 
+@pytest.mark.parametrize("W,early", [(2, 2), (2, 1), (2, 0), (4, 1), (4, 0)])
+def test_slow_consumer_rank_peers_run_ahead(W, early):
+    """Rank 0 consumes each output slowly (a long GPU sleep, then a copy, on its stream) while
+    the other ranks issue their forwards back to back: a peer's forward e+2 may start its first
+    stage early (programmatic launch) but must not store into rank 0's buffer half before rank 0
+    has copied output e out.  Every copy and every rank's outputs match the oracle."""
+    from paper_2305_06942_b200 import LoopbackGroup
+    cfg = synth.config_for("tiny", W=W, B=64)
+    probs = [from_config(cfg, k) for k in range(4)]
+    # Virtual ranks share one GPU: by default a forward then triggers its programmatic
+    # dependents only by exiting (a rank running ahead would otherwise park waiting CTAs of its
+    # next forwards on SM slots the slow rank needs).  early = 2 forces the multi-GPU behaviour
+    # (early trigger, early consumers, the held-back first stage); one CTA per SM per rank and
+    # W = 2 keep that co-resident here.
+    g = LoopbackGroup(W, dev(), {"slice": 4, "chunk": 2, "pdl_rows_early": early,
+                                 "timeout_ms": 4000, "ctas_per_sm": 1})
+    tabs = [[torch.from_numpy(t).to(dev()) for t in probs[0].rank_tables(r)] for r in range(W)]
+    g.register_tables(tabs, cfg.B, cfg.part)
+    csr = [dev_csr(pr) for pr in probs]
+    copies = {r: [] for r in range(W)}
+    # load the torch kernels used below first: a module load queued behind a forward that is
+    # waiting for a peer on this same GPU would stall that peer (lazy loading)
+    torch.cuda._sleep(10)
+    torch.zeros(4, device=dev()).clone()
+    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream()
+    for s_ in g.streams:
+        s_.wait_stream(cur)
+    last = {}
+    for e in range(4):
+        for r, h in enumerate(g.handles):
+            st = g.streams[r]
+            out = h.forward(csr[e][0][r], csr[e][1][r], stream=st)
+            last[r] = out
+            if r == 0:           # rank 0 consumes slowly; the others run forward after forward
+                with torch.cuda.stream(st):
+                    torch.cuda._sleep(20_000_000)
+                    copies[0].append(out.clone())
+    for s_ in g.streams:
+        cur.wait_stream(s_)
+    torch.cuda.synchronize()
+    for h in g.handles:
+        h.check()                    # no receive wait timed out
+    for e in range(4):
+        np.testing.assert_array_equal(copies[0][e].cpu().numpy(), oracle_out(probs[e])[0])
+    ref = oracle_out(probs[3])
+    for r in range(1, W):
+        np.testing.assert_array_equal(last[r].cpu().numpy(), ref[r])
+    g.destroy()
+
+
 def test_forward_host_back_to_back_double_buffered_staging():
     """Six forward_host calls without a sync in between (inputs of different sizes, so the
     staging regrows once; the two staging buffers alternate and each call's input copy runs on
