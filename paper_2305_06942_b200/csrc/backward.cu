@@ -613,9 +613,15 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
         else
           src = P.grad + (j * P.T + (int)t) * D;
         wsrc[lane] = reinterpret_cast<long long>(src);
-        wtab[lane] = reinterpret_cast<long long>(
-            (P.rbits >= 32) ? tabs[0] + (size_t)key * D
-                            : tabs[(int)(key >> P.rbits)] + (size_t)(key & rmask) * D);
+        float* trow = (P.rbits >= 32) ? tabs[0] + (size_t)key * D
+                                      : tabs[(int)(key >> P.rbits)] + (size_t)(key & rmask) * D;
+        wtab[lane] = reinterpret_cast<long long>(trow);
+        // a run that starts here will read and write its table row at its end: bring the row
+        // into L2 now, so the walk's round trips are L2 (gradient rows) rather than HBM
+        if (((startm >> lane) & 1u) && !(lane == 0 && in_sb))
+          for (int b = 0; b < D * 4; b += 128)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(
+                             reinterpret_cast<const char*>(trow) + b));
         if (MODE == 1) wsc[lane] = P.wts[pb + lane];
         if (MODE == 2) wsc[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
       }
