@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   __syncthreads();
   float* const* tabs = P.T <= kMaxSmemTables ? s_tab : P.tables;
 
-  // ---- reduce + update, pass 1 (R#31).  Work unit = a chunk of kBwdChunk consecutive sorted
+  // ---- reduce + update, pass 1 (R#31).  Work unit = a chunk of P.chunk consecutive sorted
   // lookups per warp, taken 32 at a time (sub-batches).  A sub-batch's runs (pieces of equal
   // keys) are split into NG contiguous ranges, one per lane group (LPG lanes cover a row); a
   // group walks its range in sorted order with UF gradient rows in flight per lane and sums each
@@ -561,8 +561,8 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   btrace(P, 21, 0);
   for (long long c = gw; c < P.nchunks;) {
     btrace(P, 22, (unsigned)c);
-    const long long p0 = c * kBwdChunk;
-    const int clen = (n - p0) < kBwdChunk ? (int)(n - p0) : kBwdChunk;
+    const long long p0 = c * P.chunk;
+    const int clen = (n - p0) < P.chunk ? (int)(n - p0) : P.chunk;
     // sub-batch 0's lookups; the keys just before and just after the chunk
     unsigned key = 0u, nkey = 0u;
     int bag = 0, nbag = 0;
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(256) bwd_fold_kernel(const __grid_constant__ B
   for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < P.nchunks;
        c += nw) {
     if (!(P.info[c] & 1)) continue;
-    const unsigned K = P.keys[c * kBwdChunk + kBwdChunk - 1];
+    const unsigned K = P.keys[c * P.chunk + P.chunk - 1];
     float4 tot[NVC];
 #pragma unroll
     for (int v = 0; v < NVC; ++v) {

@@ -214,7 +214,8 @@ struct BwdParams {
   long long B, timeout_ns;
   unsigned long long bepoch;   // 1-based fused-backward number (exchange counters, parity)
   float lr;
-  long long nchunks;           // chunks of kBwdChunk sorted lookups
+  long long nchunks;           // chunks of `chunk` sorted lookups
+  int chunk;                   // sorted lookups per pass-1 work unit (a multiple of 32)
   long long wbytes;            // shared memory per warp (finish queue)
   int flist;                   // finish-queue entries per warp
   int W, r, T, D, G, toff, rbits, fused, mean, parity;
@@ -238,6 +239,9 @@ inline int bwd_flist(int D) {
   int c = 2048 / D;
   return c > 16 ? 16 : (c < 2 ? 2 : c);
 }
-constexpr int kBwdChunk = 64;    // sorted lookups per warp work unit (2 sub-batches of 32)
+// sorted lookups per pass-1 work unit: 2 sub-batches of 32, 4 for wide rows (fewer crossing
+// runs; measured: D=256 415 vs 451 us, D<=128 best at 64)
+constexpr int kBwdChunkMin = 64;
+inline int bwd_chunk_for(int D) { return D >= 256 ? 128 : 64; }
 
 }  // namespace emba2a

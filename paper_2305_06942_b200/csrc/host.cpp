@@ -981,7 +981,8 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.D = h->D;
   P.G = h->G;
   P.toff = h->toff;
-  P.nchunks = (P.n + kBwdChunk - 1) / kBwdChunk;
+  P.chunk = bwd_chunk_for(h->D);
+  P.nchunks = (P.n + P.chunk - 1) / P.chunk;
   P.flist = 0;
   // per warp: gradient-row and table-row pointers and scalars of a sub-batch, a carried sum
   P.wbytes = 32 * (8 + 8 + 4) + 2 * (int64_t)h->D * 4;
@@ -1056,7 +1057,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   }
   const int64_t n = (h->T > 0) ? num_indices : 0;
   const int passes = (tbits + rbits + 7) / 8;
-  const int64_t nchunks = (n + kBwdChunk - 1) / kBwdChunk;
+  const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
   // plan storage (grow-only)
@@ -1352,7 +1353,7 @@ int emb_a2a_query(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "backward_epoch") *v = (int64_t)h->bepoch;
   else if (k == "plan_lookups") *v = h->planned ? h->plan_n : -1;
   else if (k == "bwd_grid") *v = h->bwd_grid;
-  else if (k == "bwd_chunk") *v = kBwdChunk;
+  else if (k == "bwd_chunk") *v = bwd_chunk_for(h->D);
   else if (k.rfind("expected_in:", 0) == 0) {
     const int q = atoi(k.c_str() + 12);
     if (q < 0 || q >= h->W) return EMB_A2A_EINVAL;
