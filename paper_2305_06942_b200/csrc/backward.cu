@@ -80,22 +80,38 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
     const int my_off = lane < nb ? S.offsets[b0 + lane] : 0x7fffffff;
     const int lo = __shfl_sync(kFull, my_off, 0);
     const int hi = S.offsets[b0 + nb];
-    for (int base = lo; base < hi; base += 32) {
-      const int p = base + lane;
-      int i = 0;
+    // the group's lookups are requested UNROLL x 32 at a time before any key is stored (the
+    // stores could alias the loads, so the compiler would not hoist them itself)
+    constexpr int UNROLL = 8;
+    for (int base0 = lo; base0 < hi; base0 += 32 * UNROLL) {
+      int ix[UNROLL];
+      float wv[UNROLL];
 #pragma unroll
-      for (int step = BPW / 2; step >= 1; step >>= 1) {
-        const int v = __shfl_sync(kFull, my_off, i + step);
-        if (i + step < nb && v <= p) i += step;
+      for (int u = 0; u < UNROLL; ++u) {
+        const int p = base0 + 32 * u + lane;
+        ix[u] = p < hi ? S.indices[p] : 0;
+        if (WEIGHTED) wv[u] = p < hi ? S.weights[p] : 0.f;
       }
-      if (p < hi) {
-        const long long bag = b0 + i;
-        const unsigned t = (unsigned)(bag / S.B);
-        const unsigned key = (S.rbits >= 32 ? 0u : (t << S.rbits)) | (unsigned)S.indices[p];
-        S.keys[p] = key;
-        S.bags[p] = (int)bag;
-        if (WEIGHTED) S.wts[p] = S.weights[p];
-        for (int q = 0; q < S.passes; ++q) atomicAdd(&h[q * 256 + ((key >> (8 * q)) & 255u)], 1u);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int p = base0 + 32 * u + lane;
+        if (base0 + 32 * u >= hi) break;            // warp-uniform
+        int i = 0;
+#pragma unroll
+        for (int step = BPW / 2; step >= 1; step >>= 1) {
+          const int v = __shfl_sync(kFull, my_off, i + step);
+          if (i + step < nb && v <= p) i += step;
+        }
+        if (p < hi) {
+          const long long bag = b0 + i;
+          const unsigned t = (unsigned)(bag / S.B);
+          const unsigned key = (S.rbits >= 32 ? 0u : (t << S.rbits)) | (unsigned)ix[u];
+          S.keys[p] = key;
+          S.bags[p] = (int)bag;
+          if (WEIGHTED) S.wts[p] = wv[u];
+          for (int q = 0; q < S.passes; ++q)
+            atomicAdd(&h[q * 256 + ((key >> (8 * q)) & 255u)], 1u);
+        }
       }
     }
   }
@@ -820,7 +836,7 @@ __global__ void __launch_bounds__(256) bwd_fold_kernel(const __grid_constant__ B
       const bool in = q + lane < P.nchunks && (P.info[q + lane] & 2);
       const unsigned m = __ballot_sync(kFull, in);
       const int k = (m == kFull) ? 32 : __ffs(~m) - 1;     // chunks q .. q+k-1 lie inside the run
-      for (int x0 = 0; x0 <= k; x0 += BATCH) {             // ... and chunk q+k ends it
+      for (int x0 = 0; x0 < (k < 32 ? k + 1 : 32); x0 += BATCH) {             // ... and chunk q+k ends it
         float4 pv[BATCH][NVC];
 #pragma unroll
         for (int x = 0; x < BATCH; ++x) {
