@@ -44,6 +44,16 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -69,6 +79,9 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
   constexpr int BPW = 8;
   __shared__ unsigned h[kMaxPasses * 256];
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) h[i] = 0u;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.lbg_words;
+       i += (long long)gridDim.x * blockDim.x)
+    S.lbg[i] = 0u;                     // the passes' group look-back words (they follow keygen)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long ngroups = (S.TB + BPW - 1) / BPW;
@@ -147,7 +160,7 @@ __device__ __forceinline__ void ptrace(const PassParams& P, unsigned event, unsi
   P.trace[3 + 2 * i] = globaltimer();
 }
 
-// Look-back words: [63:34] stamp | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] count
+// Look-back words: [63:34] stamp | [33:32] flag (1 = the tile's digit count published) | [31:0] count
 __device__ __forceinline__ unsigned long long lb_word(unsigned stamp, unsigned flag,
                                                       unsigned count) {
   return ((unsigned long long)(stamp & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) |
@@ -222,40 +235,58 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     s_cnt[ww][d] = run;
     run += c;
   }
-  unsigned long long* my = P.status + tile * 256 + d;
+  // Look-back in two levels.  Tile k of group J = k / G (G = kLbGroup tiles) publishes its
+  // digit counts twice: as its look-back word (read by the later tiles of its group) and added
+  // into the group's sums, after which one thread counts the tile in on the group's arrival
+  // counter (release).  The exclusive prefix of tile k = the sums of groups 0 .. J-1 (complete
+  // once their counters reach G) + the words of tiles J*G .. k-1.  All tiles publish at about
+  // the same time, so this is ~3 round trips; a chain of single-tile look-back windows costs
+  // ~k/16 of them.  Tiles are taken in ticket order, so every tile waited for is running and
+  // will publish; the time bound only guards against a broken invariant hanging the GPU.
+  const long long ngroups = (P.ntiles + kLbGroup - 1) / kLbGroup;
+  const long long J = tile / kLbGroup, j0 = J * kLbGroup;
+  st_relaxed_gpu(P.status + tile * 256 + d, lb_word(P.stamp, 1, run));
+  if (J + 1 < ngroups) atomicAdd(P.gsum + J * 256 + d, run);
+  __syncthreads();
+  if (tid == 0 && J + 1 < ngroups) {
+    __threadfence();
+    atomicAdd(P.garrive + J, 1u);
+  }
+  const unsigned want = P.stamp & 0x3fffffffu;
+  const unsigned long long tb = globaltimer();
   unsigned excl = 0;
-  if (tile == 0) {
-    st_relaxed_gpu(my, lb_word(P.stamp, 2, run));
-  } else {
-    st_relaxed_gpu(my, lb_word(P.stamp, 1, run));
-    // look back 8 tiles per round trip: read the window's words together, then take them in
-    // order from the nearest, stopping at the first inclusive prefix; a word not yet published
-    // is re-read alone (tiles are taken in ticket order, so every predecessor is running and
-    // will publish; the time bound only guards against a broken invariant hanging the GPU)
-    long long look = tile - 1;
-    const unsigned want = P.stamp & 0x3fffffffu;
-    const unsigned long long t0 = globaltimer();
-    bool done = false;
-    while (look >= 0 && !done) {
-      constexpr int LB = 8;
-      unsigned long long v[LB];
+  {
+    unsigned long long v[kLbGroup - 1];
 #pragma unroll
-      for (int i = 0; i < LB; ++i)
-        v[i] = (look - i >= 0) ? ld_relaxed_gpu(P.status + (look - i) * 256 + d) : 0ull;
+    for (int i = 0; i < kLbGroup - 1; ++i)
+      v[i] = (j0 + i < tile) ? ld_relaxed_gpu(P.status + (j0 + i) * 256 + d) : 0ull;
 #pragma unroll
-      for (int i = 0; i < LB; ++i) {
-        if (done || look - i < 0) continue;
-        unsigned long long w = v[i];
-        while ((unsigned)(w >> 34) != want || ((unsigned)(w >> 32) & 3u) == 0u) {
-          if (globaltimer() - t0 > 5000000000ull) break;
-          w = ld_relaxed_gpu(P.status + (look - i) * 256 + d);
-        }
-        excl += (unsigned)w;
-        if (((unsigned)(w >> 32) & 3u) == 2u) done = true;
+    for (int i = 0; i < kLbGroup - 1; ++i) {
+      if (j0 + i >= tile) continue;
+      unsigned long long w = v[i];
+      while ((unsigned)(w >> 34) != want || ((unsigned)(w >> 32) & 3u) == 0u) {
+        if (globaltimer() - tb > 5000000000ull) break;
+        w = ld_relaxed_gpu(P.status + (j0 + i) * 256 + d);
       }
-      look -= LB;
+      excl += (unsigned)w;
     }
-    st_relaxed_gpu(my, lb_word(P.stamp, 2, excl + run));
+  }
+  if (J > 0) {
+    for (long long jj = tid; jj < J; jj += kSortThreads) {
+      while (ld_acquire_gpu_u32(P.garrive + jj) < (unsigned)kLbGroup)
+        if (globaltimer() - tb > 5000000000ull) break;
+    }
+    __threadfence();
+    __syncthreads();
+    long long jj = 0;
+    for (; jj + 8 <= J; jj += 8) {
+      unsigned g[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g[i] = ld_relaxed_gpu_u32(P.gsum + (jj + i) * 256 + d);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) excl += g[i];
+    }
+    for (; jj < J; ++jj) excl += ld_relaxed_gpu_u32(P.gsum + jj * 256 + d);
   }
   // the digit's global base: exclusive scan of the pass histogram (after the look-back, so the
   // tile's aggregate is published as early as possible)

@@ -161,6 +161,7 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
 constexpr int kMaxPasses = 4;                          // 32-bit keys
+constexpr int kLbGroup = 16;                           // onesweep look-back group (tiles)
 
 struct SortParams {
   const int* indices;
@@ -172,6 +173,8 @@ struct SortParams {
   unsigned* hist;              // [kMaxPasses][256] digit counts (zeroed before keygen)
   long long TB, B;
   int rbits, passes;
+  unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)
+  long long lbg_words;
 };
 
 struct PassParams {
@@ -185,6 +188,8 @@ struct PassParams {
   unsigned* cnt;               // [256][ntiles] tile digit counts -> global digit offsets
   unsigned long long* status;  // onesweep: [ntiles][256] look-back words of this pass
   unsigned* tile_ctr;          // onesweep: this pass's tile ticket (zeroed before keygen)
+  unsigned* garrive;           // onesweep: [ngroups] tiles of each look-back group counted in
+  unsigned* gsum;              // onesweep: [ngroups][256] digit counts of each group's tiles
   long long ntiles;
   long long n;
   int shift;

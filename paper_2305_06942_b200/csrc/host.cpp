@@ -146,6 +146,8 @@ struct emb_a2a {
   unsigned* d_cnt = nullptr;             // radix pass: [256][ntiles] tile digit counts
   size_t cnt_cap = 0;
   unsigned long long* d_status = nullptr;  // onesweep look-back words
+  unsigned* d_lbg = nullptr;             // onesweep group look-back: [passes][ngroups][1 + 256]
+  size_t lbg_cap = 0;
   size_t status_cap = 0;
   float* d_scratch = nullptr;
   unsigned char* d_info = nullptr;       // per-chunk crossing-run flags (backward pass 2)
@@ -234,6 +236,8 @@ void release_registration(emb_a2a* h) {
   if (h->d_hist) cudaFree(h->d_hist);
   if (h->d_cnt) cudaFree(h->d_cnt);
   if (h->d_status) cudaFree(h->d_status);
+  if (h->d_lbg) cudaFree(h->d_lbg);
+  h->d_lbg = nullptr;
   h->d_status = nullptr;
   h->cnt_cap = 0;
   if (h->d_scratch) cudaFree(h->d_scratch);
@@ -1092,6 +1096,13 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     CUDA_TRY(h, cudaMemsetAsync(h->d_status, 0, scap * 8, st));   // ordered before the plan
     h->status_cap = scap;
   }
+  const long long ngroups = (ntiles + kLbGroup - 1) / kLbGroup;
+  const size_t nlbg = (size_t)passes * ngroups * 257;      // zeroed by keygen every plan
+  if (nlbg > h->lbg_cap) {
+    const size_t scap = nlbg + nlbg / 4 + 257;
+    if ((rc = grow(h, &h->d_lbg, scap))) return rc;
+    h->lbg_cap = scap;
+  }
   if ((size_t)nchunks > h->chunk_cap) {
     const size_t cap = (size_t)nchunks + nchunks / 4 + 64;    // headroom: batches vary in size
     if ((rc = grow(h, &h->d_scratch, cap * 2 * h->D))) return rc;
@@ -1120,6 +1131,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   S.B = h->B;
   S.rbits = rbits;
   S.passes = passes;
+  S.lbg = h->d_lbg;
+  S.lbg_words = (long long)nlbg;
   PassParams pp[kMaxPasses];
   for (int p = 0; p < passes; ++p) {
     PassParams& q = pp[p];
@@ -1134,6 +1147,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.cnt = h->d_cnt;
     q.status = h->d_status + (size_t)p * ntiles * 256;
     q.tile_ctr = h->d_hist + kMaxPasses * 256 + p;
+    q.garrive = h->d_lbg + (size_t)p * ngroups * 257;
+    q.gsum = q.garrive + ngroups;
     q.ntiles = ntiles;
     q.n = n;
     q.shift = 8 * p;
