@@ -414,11 +414,13 @@ def test_backward_rejects_half_tables_and_missing_plan():
     h.destroy()
 
 
-@pytest.mark.parametrize("name", ["dlrm_small"])
+@pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p8", "dlrm_wide"])
 def test_full_size_backward_sampled_rows(name):
     """BASELINE config at full size (W=1 per-rank work, as bench.py times it): the plan sorts
     every lookup; check the updated table on sampled rows against the oracle on just the
-    lookups of those rows (the sum over a row depends only on that row's lookups)."""
+    lookups of those rows (the sum over a row depends only on that row's lookups).  DLRM-small
+    and weak sort in one wave of onesweep tiles, sweep P=8 and DLRM-wide (1-2 M lookups) take
+    the reduce-then-scan passes; DLRM-wide (D = 256) takes 128-lookup chunks."""
     cfg = synth.config_for(name, W=1)
     csr = synth.gen_all_csr(cfg, 0)
     idx_h, off_h = csr[0]
@@ -437,13 +439,14 @@ def test_full_size_backward_sampled_rows(name):
         o = off_h[t * cfg.B:(t + 1) * cfg.B + 1]
         seg = idx_h[o[0]:o[-1]]
         uniq, cnt = np.unique(seg, return_counts=True)
-        pick = np.concatenate([uniq[np.argsort(-cnt)[:4]], rng.choice(uniq, 12, replace=False)])
+        pick = np.unique(np.concatenate([uniq[np.argsort(-cnt)[:4]], rng.choice(uniq, 12, replace=False)]))
         got = tabs[t][torch.from_numpy(pick.astype(np.int64)).to(dev())].cpu().numpy()
         # oracle on the sub-problem of just these rows (remapped to 0..len(pick)-1)
         bags = []
+        where = {int(x): k for k, x in enumerate(pick)}
         for j in range(cfg.B):
             rows = seg[o[j] - o[0]:o[j + 1] - o[0]]
-            bags.append([int(np.nonzero(pick == x)[0][0]) for x in rows if x in set(pick.tolist())])
+            bags.append([where[int(x)] for x in rows if int(x) in where])
         si, so = csr_from_bags([bags])
         sub_grad = [grad[:, t * cfg.D:(t + 1) * cfg.D]]
         want = oracle.backward_sgd([0, cfg.B], cfg.D, cfg.B, [1], [np.zeros((len(pick), cfg.D), np.float32)],
