@@ -176,6 +176,7 @@ template <bool WEIGHTS>
 __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassParams P) {
   constexpr int NW = kSortThreads / 32;
   __shared__ unsigned s_cnt[NW][256];   // running per-warp digit counts -> warp offsets in tile
+  __shared__ unsigned s_hist[256];      // the tile's digit counts
   __shared__ unsigned s_gofs[256];
   __shared__ unsigned s_tstart[256];    // first tile-local slot of each digit
   __shared__ unsigned s_warp[NW];
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   pdl_trigger();
   for (int i = tid; i < NW * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
+  s_hist[tid] = 0u;
   pdl_wait();
   if (tid == 0) s_tile = atomicAdd(P.tile_ctr, 1u);
   const unsigned hval = P.hist[tid];   // this pass's count of digit tid (for the global base)
@@ -213,38 +215,31 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     if (x == 0xdeadbeefu) s_tile = x;
     ptrace(P, 31, (unsigned)tile);
   }
+  // The tile's digit counts first (one shared add per group of equal digits in a warp), so the
+  // tile publishes them -- and the look-back of later tiles can complete -- while it ranks.
+  const long long ngroups = (P.ntiles + kLbGroup - 1) / kLbGroup;
+  const long long J = tile / kLbGroup, j0 = J * kLbGroup;
+  unsigned peers[kSortItems];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
     const unsigned d = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
-    const unsigned peers = __match_any_sync(kFull, d);
-    const unsigned c = d < 256u ? s_cnt[w][d] : 0u;
-    rank[i] = (unsigned short)(c + __popc(peers & lt_mask));
-    __syncwarp();
-    if (d < 256u && lane == __ffs(peers) - 1) s_cnt[w][d] = c + __popc(peers);
-    __syncwarp();
+    peers[i] = __match_any_sync(kFull, d);
+    if (d < 256u && lane == __ffs(peers[i]) - 1) atomicAdd(&s_hist[d], __popc(peers[i]));
   }
   __syncthreads();
-  ptrace(P, 32, (unsigned)tile);
-  // thread d: exclusive offsets of digit d per warp, the tile's count, the global base
   const unsigned d = tid;
-  unsigned run = 0;
-#pragma unroll
-  for (int ww = 0; ww < NW; ++ww) {
-    const unsigned c = s_cnt[ww][d];
-    s_cnt[ww][d] = run;
-    run += c;
-  }
+  const unsigned run = s_hist[d];      // the tile's count of digit d
   // Look-back in two levels.  Tile k of group J = k / G (G = kLbGroup tiles) publishes its
-  // digit counts twice: as its look-back word (read by the later tiles of its group) and added
-  // into the group's sums, after which one thread counts the tile in on the group's arrival
-  // counter (release).  The exclusive prefix of tile k = the sums of groups 0 .. J-1 (complete
-  // once their counters reach G) + the words of tiles J*G .. k-1.  All tiles publish at about
-  // the same time, so this is ~3 round trips; a chain of single-tile look-back windows costs
-  // ~k/16 of them.  Tiles are taken in ticket order, so every tile waited for is running and
-  // will publish; the time bound only guards against a broken invariant hanging the GPU.
-  const long long ngroups = (P.ntiles + kLbGroup - 1) / kLbGroup;
-  const long long J = tile / kLbGroup, j0 = J * kLbGroup;
+  // digit counts twice: as its stamped look-back word (read by the later tiles of its group)
+  // and added into the group's sums, after which one thread counts the tile in on the group's
+  // arrival counter (fence + add = release).  The exclusive prefix of tile k = the sums of
+  // groups 0 .. J-1 (complete once their counters reach G) + the words of tiles J*G .. k-1.
+  // All tiles publish at about the same time, so this is ~3 round trips; a chain of 8-tile
+  // look-back windows costs ~k/16 of them.  (Tried: a 64-bit word per group and digit carrying
+  // its own tile count, no fence: slower -- 256 threads polling words instead of J counters.)
+  // Tiles are taken in ticket order, so every tile waited for is running and will publish;
+  // the time bound only guards against a broken invariant hanging the GPU.
   st_relaxed_gpu(P.status + tile * 256 + d, lb_word(P.stamp, 1, run));
   if (J + 1 < ngroups) atomicAdd(P.gsum + J * 256 + d, run);
   __syncthreads();
@@ -252,14 +247,42 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     __threadfence();
     atomicAdd(P.garrive + J, 1u);
   }
+  // stable rank of each key within its warp's digit (warp-striped: item, then lane = position)
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const long long pos = base + i * 32 + lane;
+    const unsigned dd = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
+    const unsigned c = dd < 256u ? s_cnt[w][dd] : 0u;
+    rank[i] = (unsigned short)(c + __popc(peers[i] & lt_mask));
+    __syncwarp();
+    if (dd < 256u && lane == __ffs(peers[i]) - 1) s_cnt[w][dd] = c + __popc(peers[i]);
+    __syncwarp();
+  }
+  __syncthreads();
+  ptrace(P, 32, (unsigned)tile);
+  // thread d: exclusive offsets of digit d per warp
+  {
+    unsigned acc = 0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) {
+      const unsigned c = s_cnt[ww][d];
+      s_cnt[ww][d] = acc;
+      acc += c;
+    }
+  }
   const unsigned want = P.stamp & 0x3fffffffu;
   const unsigned long long tb = globaltimer();
-  unsigned excl = 0;
+  unsigned excl = 0, gbase;
   {
     unsigned long long v[kLbGroup - 1];
 #pragma unroll
     for (int i = 0; i < kLbGroup - 1; ++i)
       v[i] = (j0 + i < tile) ? ld_relaxed_gpu(P.status + (j0 + i) * 256 + d) : 0ull;
+    // while those are in flight: the digit's global base (exclusive scan of the pass
+    // histogram) and its first slot in the tile
+    gbase = block_excl_scan256(hval, s_warp);
+    __syncthreads();                     // s_warp is reused by the next scan
+    s_tstart[d] = block_excl_scan256(run, s_warp);
 #pragma unroll
     for (int i = 0; i < kLbGroup - 1; ++i) {
       if (j0 + i >= tile) continue;
@@ -276,8 +299,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
       while (ld_acquire_gpu_u32(P.garrive + jj) < (unsigned)kLbGroup)
         if (globaltimer() - tb > 5000000000ull) break;
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();                   // the acquires above order the group sums read below
     long long jj = 0;
     for (; jj + 8 <= J; jj += 8) {
       unsigned g[8];
@@ -288,12 +310,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
     }
     for (; jj < J; ++jj) excl += ld_relaxed_gpu_u32(P.gsum + jj * 256 + d);
   }
-  // the digit's global base: exclusive scan of the pass histogram (after the look-back, so the
-  // tile's aggregate is published as early as possible)
-  const unsigned gbase = block_excl_scan256(hval, s_warp);
   s_gofs[d] = gbase + excl;
-  __syncthreads();                       // s_warp is reused by the next scan
-  s_tstart[d] = block_excl_scan256(run, s_warp);
   __syncthreads();
   ptrace(P, 33, (unsigned)tile);
   // reorder the tile by digit in shared memory, then write each digit's run of keys out
