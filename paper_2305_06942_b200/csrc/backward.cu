@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.lbg_words;
        i += (long long)gridDim.x * blockDim.x)
     S.lbg[i] = 0u;                     // the passes' group look-back words (they follow keygen)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHistWords; i += gridDim.x * blockDim.x)
+    S.hist_clear[i] = 0u;              // the next plan's digit counts and tile tickets
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long ngroups = (S.TB + BPW - 1) / BPW;

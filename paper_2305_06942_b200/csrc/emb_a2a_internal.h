@@ -161,6 +161,7 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
 constexpr int kMaxPasses = 4;                          // 32-bit keys
+constexpr int kHistWords = kMaxPasses * 256 + kMaxPasses;   // digit counts + tile tickets
 constexpr int kLbGroup = 16;                           // onesweep look-back group (tiles)
 
 struct SortParams {
@@ -170,7 +171,8 @@ struct SortParams {
   unsigned* keys;              // [n] out (keygen) / pass ping-pong buffers
   int* bags;
   float* wts;
-  unsigned* hist;              // [kMaxPasses][256] digit counts (zeroed before keygen)
+  unsigned* hist;              // [kMaxPasses][256] digit counts + tile tickets (zero at entry)
+  unsigned* hist_clear;        // the other half of the plan buffer: zeroed here for the next plan
   long long TB, B;
   int rbits, passes;
   unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)

@@ -142,7 +142,9 @@ struct emb_a2a {
   int* d_bags[2] = {nullptr, nullptr};
   float* d_wts[2] = {nullptr, nullptr};
   size_t plan_cap = 0, wts_cap = 0;
-  unsigned* d_hist = nullptr;            // [kMaxPasses][256] + kMaxPasses tile tickets
+  unsigned* d_hist = nullptr;            // 2 x ([kMaxPasses][256] digit counts + kMaxPasses tile
+                                         // tickets) + the backward chunk ticket
+  int hist_par = 0;                      // the half the next plan uses (keygen zeroes the other)
   unsigned* d_cnt = nullptr;             // radix pass: [256][ntiles] tile digit counts
   size_t cnt_cap = 0;
   unsigned long long* d_status = nullptr;  // onesweep look-back words
@@ -971,7 +973,7 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.tables = (float* const*)h->d_tables;
   P.scratch = h->d_scratch;
   P.info = h->d_info;
-  P.ticket = h->d_hist + kMaxPasses * 256 + kMaxPasses;
+  P.ticket = h->d_hist + 2 * kHistWords;
   P.trace = h->d_trace;
   P.trace_cap = h->trace_cap;
   P.err = h->d_err;
@@ -1080,8 +1082,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   }
   // [pass histograms | pass tile tickets | backward chunk ticket]
   if (!h->d_hist) {
-    if ((rc = grow(h, &h->d_hist, kMaxPasses * 256 + kMaxPasses + 1))) return rc;
-    CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (kMaxPasses * 256 + kMaxPasses + 1) * 4, st));
+    if ((rc = grow(h, &h->d_hist, 2 * kHistWords + 1))) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (2 * kHistWords + 1) * 4, st));
   }
   const size_t ncnt = (size_t)ntiles * 256;      // tile digit counts of one pass
   if (ncnt > h->cnt_cap) {
@@ -1117,7 +1119,9 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   h->plan_buf = passes & 1;
   h->planned = true;
   if (n == 0) return EMB_A2A_OK;
-  CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, (kMaxPasses * 256 + kMaxPasses) * sizeof(unsigned), st));
+  // this plan's digit counts and tile tickets: the half zeroed by the previous plan's keygen (or
+  // at allocation); this keygen zeroes the other half for the next plan (no memset in the chain)
+  unsigned* const hb = h->d_hist + h->hist_par * kHistWords;
   SortParams S;
   memset(&S, 0, sizeof(S));
   S.indices = indices;
@@ -1126,7 +1130,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   S.keys = h->d_keys[0];
   S.bags = h->d_bags[0];
   S.wts = h->d_wts[0];
-  S.hist = h->d_hist;
+  S.hist = hb;
+  S.hist_clear = h->d_hist + (1 - h->hist_par) * kHistWords;
   S.TB = (long long)h->T * h->B;
   S.B = h->B;
   S.rbits = rbits;
@@ -1143,10 +1148,10 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.bags_out = h->d_bags[(p + 1) & 1];
     q.wts_in = wtd ? h->d_wts[p & 1] : nullptr;
     q.wts_out = wtd ? h->d_wts[(p + 1) & 1] : nullptr;
-    q.hist = h->d_hist + p * 256;
+    q.hist = hb + p * 256;
     q.cnt = h->d_cnt;
     q.status = h->d_status + (size_t)p * ntiles * 256;
-    q.tile_ctr = h->d_hist + kMaxPasses * 256 + p;
+    q.tile_ctr = hb + kMaxPasses * 256 + p;
     q.garrive = h->d_lbg + (size_t)p * ngroups * 257;
     q.gsum = q.garrive + ngroups;
     q.ntiles = ntiles;
@@ -1165,8 +1170,10 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
                                    (int)h->sort_mode, st);
   if (e != cudaSuccess) {
     h->planned = false;
+    cudaMemsetAsync(h->d_hist, 0, 2 * kHistWords * sizeof(unsigned), st);   // both halves clean
     return fail(h, EMB_A2A_ECUDA, "backward plan launch: %s", cudaGetErrorString(e));
   }
+  h->hist_par ^= 1;
   h->kernel_launches += 1 + passes;
   return EMB_A2A_OK;
 }
