@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
   constexpr int BPW = 8;
   __shared__ unsigned h[kMaxPasses * 256];
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) h[i] = 0u;
+  pdl_wait();     // the caller's indices/offsets and the previous plan's passes are complete
+  pdl_trigger();  // pass 0's CTAs may take their slots and wait
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.lbg_words;
        i += (long long)gridDim.x * blockDim.x)
     S.lbg[i] = 0u;                     // the passes' group look-back words (they follow keygen)
@@ -974,9 +976,11 @@ size_t bwd_smem(const BwdParams& P, int threads) {
 cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int npasses,
                              long long ntiles, int grid_keygen, int mode, cudaStream_t st) {
   if (S.TB > 0) {
-    if (S.weights) bwd_keygen_kernel<true><<<grid_keygen, 256, 0, st>>>(S);
-    else bwd_keygen_kernel<false><<<grid_keygen, 256, 0, st>>>(S);
-    cudaError_t e = cudaGetLastError();
+    SortParams s = S;
+    void* args[] = {&s};
+    const void* fn = S.weights ? reinterpret_cast<const void*>(bwd_keygen_kernel<true>)
+                               : reinterpret_cast<const void*>(bwd_keygen_kernel<false>);
+    cudaError_t e = launch_pdl(fn, (unsigned)grid_keygen, 256, 0, st, args);
     if (e != cudaSuccess) return e;
   }
   // one wave of tiles: onesweep (1 kernel per pass, short look-back); more: reduce-then-scan
