@@ -925,6 +925,76 @@ __global__ void __launch_bounds__(256) bwd_fold_kernel(const __grid_constant__ B
   }
 }
 
+// Pass 2 for rows of at most 32 float4 (D <= 128): the same fold, with the warp cut into NGF =
+// 32 / LPG lane groups (LPG lanes cover a row) that load different chunks' partials -- group g
+// takes chunks x0 + g, x0 + g + NGF, ... -- so a window of 32 chunks is one round of loads at
+// D <= 64; the partials are then added in chunk order from the loading group's lanes
+// (shuffles), every group keeping the same running sum.  Same order, same result as the
+// one-group fold.
+__global__ void __launch_bounds__(256) bwd_fold_narrow_kernel(const __grid_constant__ BwdParams P) {
+  const int lane = threadIdx.x & 31;
+  const int D = P.D, DU = D >> 2;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  pdl_wait();     // pass 1 complete: partials, info
+  pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.ticket = 0u;   // pass 1's tickets, for next time
+  const unsigned rmask = P.rbits >= 32 ? 0xffffffffu : ((1u << P.rbits) - 1u);
+  int LPG = 1;
+  while (LPG < DU) LPG <<= 1;
+  const int NGF = 32 / LPG, g = lane / LPG, col = lane - g * LPG;
+  const bool colok = col < DU;
+  constexpr int BATCH = 16;                 // loads in flight per lane
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < P.nchunks;
+       c += nw) {
+    if (!(P.info[c] & 1)) continue;
+    const unsigned K = P.keys[c * P.chunk + P.chunk - 1];
+    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (colok) add4(tot, __ldcg(reinterpret_cast<const float4*>(P.scratch + (c * 2 + 1) * D) + col));
+    long long q = c + 1;
+    bool in = q + lane < P.nchunks && (P.info[q + lane] & 2);
+    while (true) {
+      const unsigned m = __ballot_sync(kFull, in);
+      const int k = (m == kFull) ? 32 : __ffs(~m) - 1;     // chunks q .. q+k-1 lie inside the run
+      const int kend = k < 32 ? k + 1 : 32;                // ... and chunk q+k ends it (if k < 32)
+      if (k == 32)                                         // the next window's flags, early
+        in = q + 32 + lane < P.nchunks && (P.info[q + 32 + lane] & 2);
+      for (int x0 = 0; x0 < kend; x0 += BATCH * NGF) {
+        float4 pv[BATCH];
+#pragma unroll
+        for (int s_ = 0; s_ < BATCH; ++s_) {
+          const int x = x0 + s_ * NGF + g;
+          const float* src = P.scratch + ((q + x) * 2 + (x < k ? 1 : 0)) * D;
+          pv[s_] = (x < kend && colok) ? __ldcg(reinterpret_cast<const float4*>(src) + col)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int s_ = 0; s_ < BATCH; ++s_) {
+          if (x0 + s_ * NGF >= kend) break;                // warp-uniform
+          for (int gg = 0; gg < NGF; ++gg) {
+            if (x0 + s_ * NGF + gg >= kend) break;         // warp-uniform
+            const int from = gg * LPG + col;
+            float4 v;
+            v.x = __shfl_sync(kFull, pv[s_].x, from);
+            v.y = __shfl_sync(kFull, pv[s_].y, from);
+            v.z = __shfl_sync(kFull, pv[s_].z, from);
+            v.w = __shfl_sync(kFull, pv[s_].w, from);
+            add4(tot, v);
+          }
+        }
+      }
+      if (k < 32) break;
+      q += 32;
+    }
+    float* tp = (P.rbits >= 32) ? P.tables[0] + (size_t)K * D
+                                : P.tables[(int)(K >> P.rbits)] + (size_t)(K & rmask) * D;
+    if (g == 0 && colok) {
+      float4 w = __ldcg(reinterpret_cast<const float4*>(tp) + col);
+      sgd4(w, P.lr, tot);
+      st_f4(tp + 4 * col, w);
+    }
+  }
+}
+
 typedef void (*BwdFn)(const BwdParams);
 
 template <int NVC>
@@ -948,7 +1018,7 @@ BwdFn pick_bwd(const BwdParams& P) {
 
 BwdFn pick_fold(const BwdParams& P) {
   const int nvc = (P.D / 4 + 31) / 32;
-  return nvc <= 1 ? bwd_fold_kernel<1> : nvc <= 2 ? bwd_fold_kernel<2>
+  return nvc <= 1 ? bwd_fold_narrow_kernel : nvc <= 2 ? bwd_fold_kernel<2>
        : nvc <= 4 ? bwd_fold_kernel<4> : bwd_fold_kernel<8>;
 }
 
