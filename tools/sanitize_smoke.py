@@ -20,10 +20,14 @@ ap.add_argument("--W", type=int, default=1)
 args = ap.parse_args()
 dev = torch.device("cuda:0")
 cases = [({}, "sum"), ({"tma": 1}, "sum"), ({"flat_below": 1000}, "sum"), ({"vec": 2}, "mean"),
-         ({"idx_cap": 3}, "sum"), ({"tma": 1, "stage_kb": 1}, "sum")]
+         ({"idx_cap": 3}, "sum"), ({"tma": 1, "stage_kb": 1}, "sum"),
+         ({}, "sum")]   # 60 K lookups: 30 sort tiles (two look-back groups), long runs
 n = 0
 for seed, (opts, pooling) in enumerate(cases):
-    p = random_problem(900 + seed, W=args.W, value_mode=1, max_B=64, max_D=64)
+    if seed == 6:
+        p = random_problem(2004, W=args.W, value_mode=1, max_B=2048, max_D=64)
+    else:
+        p = random_problem(900 + seed, W=args.W, value_mode=1, max_B=64, max_D=64)
     if args.W > 1:
         opts = dict(opts, timeout_ms=120000)
     g = LoopbackGroup(p.W, dev, opts)
