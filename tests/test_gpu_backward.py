@@ -414,6 +414,46 @@ def test_backward_rejects_half_tables_and_missing_plan():
     h.destroy()
 
 
+def test_plans_in_any_sequence_use_clean_buffers():
+    """The plan's digit counts and tile tickets live in two halves, each keygen zeroing the
+    other half for the next plan (no memset in the plan chain).  Plans replaced before any
+    backward, empty plans in between (no keygen), and plans big enough for several onesweep
+    tiles and two look-back groups must each leave the next plan a clean half: every backward
+    matches the oracle bitwise (exact-int) for the plan it follows."""
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    rng = np.random.default_rng(5)
+    D, B, T, R = 8, 512, 4, 300
+    tab0 = [rng.integers(-8, 8, (R, D)).astype(np.float32) for _ in range(T)]
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    tabs = [torch.from_numpy(t).to(dev()) for t in tab0]
+    h.register_tables(tabs, B)
+
+    def csr(maxL):
+        bags = [[list(rng.integers(0, R, rng.integers(0, maxL + 1))) for _ in range(B)]
+                for _ in range(T)]
+        return csr_from_bags(bags)
+
+    plans = {"small": csr(3), "big": csr(40), "empty": csr(0)}
+    assert plans["big"][0].size > 16 * 2048      # > 16 onesweep tiles: two look-back groups
+    d_in = {k: (torch.from_numpy(i).to(dev()), torch.from_numpy(o).to(dev()))
+            for k, (i, o) in plans.items()}
+    want = [t.copy() for t in tab0]
+    seq = [["small", "big"], ["empty", "big"], ["big", "empty", "small"], ["big"], ["big", "big"],
+           ["empty", "empty", "small"], ["small"]]
+    for step, names in enumerate(seq):
+        for nm in names:
+            h.backward_plan(*d_in[nm])
+        last = names[-1]
+        grad = rng.integers(-4, 4, (B, T * D)).astype(np.float32)
+        h.backward(torch.from_numpy(grad).to(dev()), 0.5)
+        i, o = plans[last]
+        want = oracle.backward_sgd([0, B], D, B, [T], want, [i], [o], [grad], 0.5)
+        torch.cuda.synchronize()
+        for a, b in zip(tabs, want):
+            np.testing.assert_array_equal(a.cpu().numpy(), b, err_msg=f"step {step} {names}")
+    h.destroy()
+
+
 @pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p8", "dlrm_wide"])
 def test_full_size_backward_sampled_rows(name):
     """BASELINE config at full size (W=1 per-rank work, as bench.py times it): the plan sorts
