@@ -175,7 +175,7 @@ def oracle_pass(cfg, csr, rows_per_call=None):
 def cpu_baseline(cfg, csr_batches, budget_s):
     """Bounded sample: whole-batch oracle passes over the rotating batches until ~budget_s."""
     lookups, secs, passes = 0, 0.0, 0
-    while secs < budget_s and passes < 64:
+    while secs < budget_s and passes < 256:
         l, s = oracle_pass(cfg, csr_batches[passes % len(csr_batches)])
         lookups += l
         secs += s
