@@ -179,6 +179,7 @@ __device__ __forceinline__ unsigned long long lb_word(unsigned stamp, unsigned f
 template <bool WEIGHTS>
 __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassParams P) {
   constexpr int NW = kSortThreads / 32;
+  static_assert(kSortThreads == 256, "one thread per 8-bit digit");
   __shared__ unsigned s_cnt[NW][256];   // running per-warp digit counts -> warp offsets in tile
   __shared__ unsigned s_hist[256];      // the tile's digit counts
   __shared__ unsigned s_gofs[256];
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(256) bwd_scan_kernel(const PassParams P) {
 template <bool WEIGHTS>
 __global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassParams P) {
   constexpr int NW = kSortThreads / 32;
+  static_assert(kSortThreads == 256, "one thread per 8-bit digit");
   __shared__ unsigned s_cnt[NW][256];   // running per-warp digit counts -> warp offsets in tile
   __shared__ unsigned s_gofs[256];
   __shared__ unsigned s_tstart[256];    // first tile-local slot of each digit
