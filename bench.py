@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--pooling", default="sum", choices=["sum", "mean"], help="f2: mean pooling")
     ap.add_argument("--weighted", action="store_true", help="f2: per-sample weights")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-alpha0", action="store_true",
+                    help="skip the alpha = 0 (uniform, cold-cache) control leg")
+    ap.add_argument("--alpha0-batches", type=int, default=4)
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -150,39 +153,78 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- oracle timing
 
-def oracle_pass(cfg, csr, rows_per_call=None):
-    """The oracle as it stands (single-threaded C): this rank-0 view of the workload = every
-    destination row of every rank's output, procedural tables.  Returns (lookups, seconds)."""
+def host_cpu():
+    """The host's CPU model and logical core count (stated beside every oracle timing)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cpu": model, "host_cpu_count": os.cpu_count()}
+
+
+def oracle_rows_pass(cfg, csr, s, rows=None, weights=None, pooling="sum"):
+    """The oracle as it stands (single-threaded C, procedural tables): rank s's output rows
+    (all b_s of them, or `rows`), computed from every rank's CSR.  Returns (lookups, seconds)."""
     import oracle
     idx = [c[0] for c in csr]
     off = [c[1] for c in csr]
-    lookups, secs = 0, 0.0
-    for s in range(cfg.W):
-        b = int(cfg.part[s + 1] - cfg.part[s])
-        sel = np.arange(b) if rows_per_call is None else np.arange(min(b, rows_per_call))
-        t0 = time.perf_counter()
-        oracle.emb_a2a_rows(cfg.table_seed, cfg.value_mode, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
-                            idx, off, s, sel, check_inputs=False)
-        secs += time.perf_counter() - t0
-        for r in range(cfg.W):
-            o = off[r].astype(np.int64)
-            for t in range(cfg.T[r]):
-                js = cfg.part[s] + sel
-                lookups += int((o[t * cfg.B + js + 1] - o[t * cfg.B + js]).sum())
+    b = int(cfg.part[s + 1] - cfg.part[s])
+    sel = np.arange(b) if rows is None else np.asarray(rows, np.int64)
+    t0 = time.perf_counter()
+    oracle.emb_a2a_rows(cfg.table_seed, cfg.value_mode, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
+                        idx, off, s, sel, check_inputs=False, weights=weights,
+                        pooling=oracle.MEAN if pooling == "mean" else oracle.SUM)
+    secs = time.perf_counter() - t0
+    lookups = 0
+    js = cfg.part[s] + sel
+    for r in range(cfg.W):
+        o = off[r].astype(np.int64)
+        for t in range(cfg.T[r]):
+            lookups += int((o[t * cfg.B + js + 1] - o[t * cfg.B + js]).sum())
     return lookups, secs
 
 
-def cpu_baseline(cfg, csr_batches, budget_s):
-    """Bounded sample: whole-batch oracle passes over the rotating batches until ~budget_s."""
+def oracle_pass(cfg, csr, rows_per_call=None):
+    """Every destination's rows (the whole forward of all W ranks): the reference arm."""
+    lookups, secs = 0, 0.0
+    for s in range(cfg.W):
+        b = int(cfg.part[s + 1] - cfg.part[s])
+        rows = None if rows_per_call is None else np.arange(min(b, rows_per_call))
+        l, t = oracle_rows_pass(cfg, csr, s, rows)
+        lookups += l
+        secs += t
+    return lookups, secs
+
+
+def cpu_baseline(cfg, rank, N, csr_batches, budget_s, gather, weights=None, pooling="sum"):
+    """Bounded sample, every rank in parallel on its own host core: whole-output oracle passes
+    for THIS rank's rows over the given batches until ~budget_s.  value = all ranks' lookups /
+    the slowest rank's seconds (N single-threaded processes, N cores); single_core_value =
+    lookups / summed seconds."""
     lookups, secs, passes = 0, 0.0, 0
     while secs < budget_s and passes < 256:
-        l, s = oracle_pass(cfg, csr_batches[passes % len(csr_batches)])
+        k = passes % len(csr_batches)
+        l, t = oracle_rows_pass(cfg, csr_batches[k], rank,
+                                weights=None if weights is None else weights[k], pooling=pooling)
         lookups += l
-        secs += s
+        secs += t
         passes += 1
-    return {"value": lookups / secs, "unit": "lookups/s", "cores": 1, "kind": "oracle",
-            "sample": f"{passes} full forward(s) of the workload ({lookups} lookups, "
-                      f"{secs:.2f} s, single-threaded C oracle, procedural tables)"}
+    per = gather([float(lookups), secs, float(passes)])
+    tot_l = sum(p[0] for p in per)
+    tot_s = sum(p[1] for p in per)
+    max_s = max(p[1] for p in per)
+    return dict({"value": tot_l / max_s, "unit": "lookups/s", "cores": N, "kind": "oracle",
+                 "single_core_value": tot_l / tot_s,
+                 "per_rank": [{"lookups": int(p[0]), "seconds": p[1], "passes": int(p[2])}
+                              for p in per],
+                 "sample": f"each of {N} rank process(es) ran the single-threaded C oracle over "
+                           f"all of its own output rows (procedural tables) for ~{budget_s:g} s: "
+                           f"{int(tot_l)} lookups, {tot_s:.2f} core-seconds"}, **host_cpu())
 
 
 def run_reference(args):
@@ -209,9 +251,10 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "global_batch": cfg.B,
                        "tables_per_rank": cfg.T[0], "rows": cfg.R, "dim": cfg.D},
-            "cpu_baseline": {"value": v, "unit": "lookups/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} full forwards of the workload (all W ranks' "
-                                       "outputs), single-threaded C oracle"},
+            "cpu_baseline": dict({"value": v, "unit": "lookups/s", "cores": 1, "kind": "oracle",
+                                  "sample": f"{args.steps} full forwards of the workload (all W "
+                                            "ranks' outputs), single-threaded C oracle"},
+                                 **host_cpu()),
             "e2e": {"value": v, "unit": "lookups/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -257,14 +300,11 @@ def main():
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cfg = synth.config_for(args.config, W=N, alpha=args.alpha)
-    # ---- inputs (all resident in HBM before timing; 8 rotating batches)
-    csr_batches = [synth.gen_all_csr(cfg, k) if rank == 0 and not args.no_cpu and N == 1
-                   else None for k in range(args.batches)]
-    mine = []
-    for k in range(args.batches):
-        idx, off = (csr_batches[k][rank] if csr_batches[k] is not None
-                    else synth.gen_rank_csr(cfg, rank, k))
-        mine.append((idx, off))
+    # ---- inputs (all resident in HBM before timing; rotating batches).  Batch 0 of EVERY rank
+    # is generated here too: the oracle needs all ranks' bags for this rank's output rows
+    # (parity check, cpu_baseline).
+    csr0_all = synth.gen_all_csr(cfg, 0)
+    mine = [csr0_all[rank]] + [synth.gen_rank_csr(cfg, rank, k) for k in range(1, args.batches)]
     d_in = [(torch.from_numpy(i).to(dev), torch.from_numpy(o).to(dev)) for i, o in mine]
     h_in = [(torch.from_numpy(i).pin_memory(), torch.from_numpy(o).pin_memory()) for i, o in mine]
     nnz_all = []   # global lookups per batch
@@ -396,6 +436,39 @@ def main():
                "note": "L2 flushed (512 MiB write) + device barrier before each step, CUDA events "
                        "around each forward (includes ~5 us event overhead per step)"}
 
+    # ---- parity (outside every timed region, before the backward section updates the
+    # tables): a fresh forward of batch 0, >= 96 sampled output rows of THIS rank recomputed one
+    # by one by the oracle from every rank's bags; a mismatch fails the run
+    w_all0 = None
+    if args.weighted:
+        w_all0 = [synth.gen_weights(cfg, r, csr0_all[r][0].size, batch=0) for r in range(N)]
+    parity = parity_check(args, cfg, h, csr0_all, w_all0, rank, dev, stream, d_in[0],
+                          None if d_w is None else d_w[0])
+
+    # ---- the same step against compulsory bytes and DRAM traffic, and the alpha = 0 control
+    esize = 4 if args.table_dtype == "f32" else 2
+    comp_b = float(np.mean([compulsory_bytes(cfg, rank, mine[k % args.batches][0],
+                                             mine[k % args.batches][1], esize, args.weighted)
+                            for k in range(min(args.steps, args.batches))]))
+    kern_s = ms_step / 1e3
+    roof["compulsory_bytes_per_launch"] = comp_b
+    roof["frac_compulsory"] = comp_b / kern_s / 1e9 / peak_hbm
+    roof["dram_frac"] = (roof["traffic"] / kern_s / 1e9 / peak_hbm) if roof["traffic"] else None
+    roof["readings"] = ("frac: algorithmic bytes (every lookup's row counted, SURVEY 8(d)); "
+                        "frac_compulsory: distinct (table,row) rows + indices + offsets + "
+                        "receive buffer; dram_frac: ncu dram__bytes of the committed capture "
+                        "(cold, serialised) over this run's step time")
+    alpha0 = None
+    if not args.no_alpha0 and args.alpha != 0.0:
+        alpha0 = alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks,
+                            peak_hbm, esize)
+    nvl = None
+    if N > 1 and not shared:
+        nvl = nvlink_probe(h, N, stream, max_over_ranks)
+        if nvl and nvl.get("tx_gbs_per_gpu") and roof["bound"] == "nvlink":
+            roof["peak_measured_probe"] = nvl["tx_gbs_per_gpu"]
+            roof["frac_vs_probe"] = roof["achieved"] / nvl["tx_gbs_per_gpu"]
+
     # ---- end to end through the public API: pinned host inputs -> device -> host result
     b = h.b
     h_out = torch.empty((b, h.G * h.D), dtype=torch.float32).pin_memory()
@@ -475,8 +548,11 @@ def main():
                                     b2b_loop, max_over_ranks, peak_hbm, peak_src, d_w)
 
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, [c for c in csr_batches if c is not None], args.cpu_seconds)
+    if not args.no_cpu:
+        budget = args.cpu_seconds if N == 1 else args.cpu_seconds / 2
+        cpu = cpu_baseline(cfg, rank, N, [csr0_all], budget,
+                           lambda v: all_gather_floats(v, dist, shared, dev),
+                           weights=None if w_all0 is None else [w_all0], pooling=args.pooling)
 
     line = {
         "metric": METRIC,
@@ -505,6 +581,7 @@ def main():
                    "CUDA events around each forward after L2 flush + device barrier; sum over K; "
                    "max over ranks"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
+        "parity": parity, "alpha0": alpha0, "nvlink_probe": nvl,
         "flushed": flushed, "clocks": clocks, "gpu_launches": int(launches),
         "backward": backward,
     }
@@ -516,9 +593,12 @@ def main():
         if args.out:
             with open(args.out, "a") as f:
                 f.write(s + "\n")
+    ok = parity is None or parity.get("skipped") or parity["within_tol"]
     h.destroy()
     dist.barrier()
     dist.destroy_process_group()
+    if not ok:
+        raise SystemExit(f"rank {rank}: fused output differs from the oracle: {parity}")
 
 
 def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b_loop,
@@ -600,6 +680,105 @@ def backward_section(args, cfg, h, d_in, mine, dev, stream, N, rank, shared, b2b
                          "traffic": ncu_traffic(cfg, "_backward") if (
                              d_w is None and args.pooling == "sum" and args.alpha == 1.05) else None,
                          "distinct_rows": int(uniq), "nvlink_tx_bytes": int(tx)}}
+
+
+def all_gather_floats(vals, dist, shared, dev):
+    """Every rank's list of floats, rank-ordered."""
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared else dev)
+    outs = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(outs, t)
+    return [o.cpu().tolist() for o in outs]
+
+
+def parity_check(args, cfg, h, csr_all, w_all, rank, dev, stream, d_in0, d_w0, nsample=96):
+    """A fresh fused forward of batch 0; nsample output rows of this rank (first, last, random)
+    against the oracle, element by element: max |err|, bitwise, within the north-star
+    tolerance (|err| <= 1e-6 + 1e-5 |ref|)."""
+    import torch
+    import oracle
+    if args.table_dtype != "f32":
+        return {"skipped": "16-bit tables hold rounded procedural values; the bench's parity "
+                           "check needs the oracle's exact fp32 tables (tests cover bf16/fp16)"}
+    out = h.forward(d_in0[0], d_in0[1], stream, per_sample_weights=d_w0).clone()
+    torch.cuda.synchronize()
+    b = h.b
+    if b == 0:
+        return {"rows": 0, "max_abs_err": 0.0, "bitwise": True, "within_tol": True}
+    rng = np.random.default_rng(1000 + rank)
+    sel = np.unique(np.concatenate([[0, b - 1], rng.integers(0, b, max(nsample - 2, 0))]))
+    while sel.size < min(nsample, b):
+        sel = np.unique(np.concatenate([sel, rng.integers(0, b, nsample)]))[:min(nsample, b)]
+    t0 = time.perf_counter()
+    ref = oracle.emb_a2a_rows(cfg.table_seed, cfg.value_mode, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
+                              [c[0] for c in csr_all], [c[1] for c in csr_all], rank, sel,
+                              check_inputs=False, weights=w_all,
+                              pooling=oracle.MEAN if args.pooling == "mean" else oracle.SUM)
+    secs = time.perf_counter() - t0
+    got = out[torch.from_numpy(sel).to(dev)].cpu().numpy()
+    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    tol = 1e-6 + 1e-5 * np.abs(ref.astype(np.float64))
+    return {"rows": int(sel.size), "cols": int(ref.shape[1]), "max_abs_err": float(err.max()),
+            "bitwise": bool(np.array_equal(got.view(np.uint32), ref.view(np.uint32))),
+            "within_tol": bool((err <= tol).all()), "oracle_seconds": secs,
+            "what": "fresh fused forward of batch 0; sampled rows of this rank's output vs "
+                    "oracle.emb_a2a_rows (every rank checks its own; the line shows rank 0's)"}
+
+
+def compulsory_bytes(cfg, r, idx, off, esize=4, weighted=False):
+    """Bytes one forward cannot avoid moving: each DISTINCT (table, row) once + indices (+
+    weights) + offsets + this rank's receive buffer (SURVEY 8(d) "Zipf caveat")."""
+    T = cfg.T[r]
+    b = int(cfg.part[r + 1] - cfg.part[r])
+    uniq = sum(np.unique(idx[off[t * cfg.B]:off[(t + 1) * cfg.B]]).size for t in range(T))
+    return uniq * cfg.D * esize + idx.size * (8 if weighted else 4) + (T * cfg.B + 1) * 4 + \
+        b * cfg.G * cfg.D * 4
+
+
+def alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks, peak_hbm, esize):
+    """The same fused step on uniform indices (alpha = 0: no Zipf reuse, the cold-cache control
+    of SURVEY 8(d)), args.alpha0_batches rotating batches, timed like the headline."""
+    import torch
+    import synth
+    cfg0 = synth.config_for(args.config, W=N, alpha=0.0)
+    nb = max(1, args.alpha0_batches)
+    mine0 = [synth.gen_rank_csr(cfg0, rank, k) for k in range(nb)]
+    d0 = [(torch.from_numpy(i).to(dev), torch.from_numpy(o).to(dev)) for i, o in mine0]
+    torch.cuda.synchronize()
+    step = lambda k: h.forward(d0[k % nb][0], d0[k % nb][1], stream)  # noqa: E731
+    ms = max_over_ranks(b2b_loop(step, args.steps, args.warmup)) / args.steps
+    nnz = float(np.mean([mine0[k % nb][0].size for k in range(args.steps)]))
+    hbm_b, _ = algorithmic_bytes(cfg0, rank, nnz, esize, False)
+    comp = float(np.mean([compulsory_bytes(cfg0, rank, i, o, esize) for i, o in mine0]))
+    del d0
+    return {"us_per_step": ms * 1e3, "frac": hbm_b / (ms / 1e3) / 1e9 / peak_hbm,
+            "frac_compulsory": comp / (ms / 1e3) / 1e9 / peak_hbm,
+            "algorithmic_bytes_per_launch": hbm_b, "compulsory_bytes_per_launch": comp,
+            "batches": nb, "note": "uniform indices (alpha = 0), unweighted sum, same tables"}
+
+
+def nvlink_probe(h, N, stream, max_over_ranks, nbytes=8 << 20, reps=5):
+    """SM-issued st.global.v4 stores from every rank into every peer at once (the fused
+    kernel's store pattern without the gather): TX GB/s per GPU, max over ranks, best of reps."""
+    import torch
+    best = None
+    used = 0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h.device_barrier(stream)
+        a.record(stream)
+        used = h.peer_store_probe(nbytes, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(a.elapsed_time(b))
+        best = t if best is None else min(best, t)
+    if not used or not best:
+        return None
+    gbs = (N - 1) * used / (best / 1e3) / 1e9
+    return {"tx_gbs_per_gpu": gbs, "bytes_per_peer": used, "peers": N - 1, "ms": best,
+            "frac_of_nominal_900": gbs / 900.0, "guide_peer_copy_gbs": NVLINK_GBS,
+            "what": "one kernel, all SMs, 16-B peer stores to all N-1 peers concurrently "
+                    "(emb_a2a_peer_store_probe), CUDA events, max over ranks, best of %d" % reps}
 
 
 def working_set_mb(cfg, idx, off):

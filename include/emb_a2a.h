@@ -108,7 +108,10 @@ int emb_a2a_register_tables_ex(emb_a2a_t* h, int num_local_tables, const void* c
  *  out_rows, out_cols  receive b_r and G*D (either may be NULL).
  * Preconditions (fast path, unchecked unless set_option("validate",1)): indices in range,
  * offsets well formed.  The consumer of *out must be ordered before this rank's forward after
- * next (same stream, or an event) -- DESIGN.md "Buffer-reuse proof". */
+ * next (same stream, or an event the stream waits for): a forward adds a credit to every peer
+ * when it starts, and no peer stores into this rank's receive half before the credit of the
+ * forward that reuses it.  Exception: when a peer runs on this same GPU
+ * (virtual ranks, a test mode) the consumer must be ordered before the NEXT forward. */
 int emb_a2a_forward(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
                     int64_t num_indices, void* stream, float** out, int64_t* out_rows,
                     int64_t* out_cols);
@@ -203,6 +206,17 @@ int emb_a2a_backward_local(emb_a2a_t* h, const float* grad_mp, float lr, void* s
  * start of timed regions across GPUs.  Timeout -> ETIMEOUT on the next call. */
 int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
 
+/* NVLink store probe (benchmark tooling, not part of the op): enqueue on `stream` one kernel in
+ * which every CTA issues 16-byte st.global.v4 stores -- the fused kernel's store -- into the
+ * receive regions of ALL peers at once (512-byte runs, destinations staggered as in row a1).
+ * Writes min(bytes_per_peer, the smallest peer region) rounded down to 512 B per peer
+ * (*bytes_used); the peers' receive buffers (both halves) are overwritten, so no earlier
+ * forward output may still be in use anywhere.  Timed with events by the caller, all ranks
+ * together (after a device barrier), it gives the SM-issued peer-store bandwidth the fused
+ * kernel's exchange can reach.  W = 1: enqueues nothing, *bytes_used = 0. */
+int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
+                             int64_t* bytes_used);
+
 /* Tunables (not collective, but keep them identical on all ranks; "slice" must be):
  *   "slice"        S, pooled vectors per slice, >= 1 (P:147 user parameter; default 32)
  *   "order"        0 comm-aware staggered (default), 1 comm-aware ascending, 2 oblivious
@@ -226,9 +240,10 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *                  writes tables or this forward's receive buffer).  Set 0 if a
  *                  kernel of your own that writes the tables and triggers programmatic launch
  *                  (griddepcontrol.launch_dependents) can directly precede a forward on its stream.
- *                  With peers, the first stage for a peer is held until that peer has provably
- *                  consumed the buffer half it overwrites; off when a peer shares this GPU (its
- *                  CTAs could need the slots), 2 = on even then (tests, small grids)
+ *                  With peers, stores into a peer wait for that peer's credit (it has started
+ *                  the same forward, so it consumed the buffer half they overwrite); off when a
+ *                  peer shares this GPU (its CTAs could need the slots), 2 = on even then
+ *                  (tests, small grids)
  *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
  *                  fewer lanes per bag keeps more bags in flight per warp
  *   "tma"          0 = per-lane 16-byte LDG row gathers, indices staged in shared memory (default)
@@ -247,11 +262,14 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream);
  *   "sort_mode"    backward plan's radix passes: 0 auto (default: one kernel per pass with
  *                  look-back while the tiles fit one wave, else three kernels per pass,
  *                  reduce-then-scan), 1 always one kernel, 2 always three (results identical)
- *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 256] (default 128)
+ *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 128] (default 128;
+ *                  the kernel is compiled with __launch_bounds__(128))
  *   "bwd_share"    divide the backward's persistent grid by this (default 1): W virtual ranks on
  *                  one GPU must all be resident at once (loopback sets it to W)
  *   "debug_delay_ns"  test knob: CTAs sleep this long before signalling (stress tests)
- *   "debug_skip_signal_to"  test knob: never signal rank v (>= 0), to exercise ETIMEOUT */
+ *   "debug_skip_signal_to"  test knob: never signal rank v (>= 0), to exercise ETIMEOUT
+ *   "debug_sort_stall"  test knob: the backward plan's first radix tile publishes a stale
+ *                  look-back word (onesweep passes), so the look-back times out -> ETIMEOUT */
 int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t value);
 int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* value);
 
@@ -283,8 +301,8 @@ int emb_a2a_read_trace(emb_a2a_t* h, uint64_t* out, int64_t capacity, int64_t* n
 int emb_a2a_destroy(emb_a2a_t* h);
 
 /* Poll the asynchronous error word (not collective, no GPU work): EMB_A2A_ETIMEOUT if a receive
- * wait / backward exchange wait / barrier timed out since the last check (the handle is then
- * poisoned), EMB_A2A_ESTATE if it already was, else OK.  Synchronise the stream first to see
+ * wait / credit wait / backward exchange wait / sort look-back / barrier timed out since the
+ * last check (the handle is then poisoned), EMB_A2A_ESTATE if it already was, else OK.  Synchronise the stream first to see
  * the failures of work enqueued on it. */
 int emb_a2a_check(emb_a2a_t* h);
 

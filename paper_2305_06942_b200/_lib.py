@@ -48,6 +48,7 @@ _SIGS = {
     "emb_a2a_backward": (_I, [_P, _P, ctypes.c_float, _P]),
     "emb_a2a_backward_local": (_I, [_P, _P, ctypes.c_float, _P]),
     "emb_a2a_device_barrier": (_I, [_P, _P]),
+    "emb_a2a_peer_store_probe": (_I, [_P, _I64, _P, _PI64]),
     "emb_a2a_check": (_I, [_P]),
     "emb_a2a_set_option": (_I, [_P, ctypes.c_char_p, _I64]),
     "emb_a2a_get_option": (_I, [_P, ctypes.c_char_p, _PI64]),

@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   // its own tile count, no fence: slower -- 256 threads polling words instead of J counters.)
   // Tiles are taken in ticket order, so every tile waited for is running and will publish;
   // the time bound only guards against a broken invariant hanging the GPU.
-  st_relaxed_gpu(P.status + tile * 256 + d, lb_word(P.stamp, 1, run));
+  // (debug option "debug_sort_stall": tile 0 publishes a stale stamp, so the later tiles of its
+  // group never see it -- the look-back must then time out with an error, not hang or go on)
+  st_relaxed_gpu(P.status + tile * 256 + d,
+                 lb_word(P.stall && tile == 0 ? P.stamp + 1u : P.stamp, 1, run));
   if (J + 1 < ngroups) atomicAdd(P.gsum + J * 256 + d, run);
   __syncthreads();
   if (tid == 0 && J + 1 < ngroups) {
@@ -293,7 +296,10 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
       if (j0 + i >= tile) continue;
       unsigned long long w = v[i];
       while ((unsigned)(w >> 34) != want || ((unsigned)(w >> 32) & 3u) == 0u) {
-        if (globaltimer() - tb > 5000000000ull) break;
+        if (globaltimer() - tb > (unsigned long long)P.timeout_ns) {
+          atomicExch(P.err, 0x4000);   // a broken invariant: report it (ETIMEOUT, handle poisoned)
+          break;
+        }
         w = ld_relaxed_gpu(P.status + (j0 + i) * 256 + d);
       }
       excl += (unsigned)w;
@@ -302,7 +308,10 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   if (J > 0) {
     for (long long jj = tid; jj < J; jj += kSortThreads) {
       while (ld_acquire_gpu_u32(P.garrive + jj) < (unsigned)kLbGroup)
-        if (globaltimer() - tb > 5000000000ull) break;
+        if (globaltimer() - tb > (unsigned long long)P.timeout_ns) {
+          atomicExch(P.err, 0x4000);
+          break;
+        }
     }
     __syncthreads();                   // the acquires above order the group sums read below
     long long jj = 0;
@@ -538,17 +547,40 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
   btrace(P, 20, 0);
   // ---- exchange (fused, W > 1): push this rank's gradient rows to their table owners
   if (P.fused && P.W > 1) {
+    // buffer-reuse credit: this backward has passed its wait, so every earlier kernel on the
+    // stream -- our backward bepoch - 1, which read the staging half the peers fill next -- is
+    // complete
+    if (blockIdx.x == 0 && tid < P.W && tid != P.r)
+      red_release_sys_add(P.peers->bcredit_out[tid], 1ull);
     for (int q = tid; q < P.W; q += blockDim.x) s_pushed[q] = 0u;
     __syncthreads();
     const long long b_r = P.part[P.r + 1] - P.part[P.r];
     const long long total = (long long)(P.W - 1) * b_r;
     const long long gw = (long long)blockIdx.x * nw + warp, nwt = (long long)gridDim.x * nw;
+    int cred_ok = -1;
     for (long long m = gw; m < total; m += nwt) {
       const int k = (int)(m / b_r);
       const long long i = m - k * b_r;
       const int q = (P.r + 1 + k) % P.W;          // staggered destinations (R#19)
       const int Tq = P.allT[q];
       if (Tq == 0) continue;
+      if (q != cred_ok) {
+        // owner q's staging half bepoch & 1 was last read by q's backward bepoch - 2; q's
+        // backward bepoch - 1 having passed its wait proves that one complete
+        if (lane == 0) {
+          const unsigned long long* f = P.bcredits_in + (size_t)q * kFlagStride;
+          const unsigned long long t0 = globaltimer();
+          while (ld_acquire_sys(f) + 1ull < P.bepoch) {
+            if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
+              atomicExch(P.err, 0x2000 | q);
+              break;
+            }
+            __nanosleep(128);
+          }
+        }
+        __syncwarp();
+        cred_ok = q;
+      }
       const float4* src = reinterpret_cast<const float4*>(P.grad + (i * P.G + P.tofs[q]) * D);
       float* dst = P.peers->gstage[q][P.parity] + (P.part[P.r] + i) * Tq * (long long)D;
       const int n4 = Tq * DU;

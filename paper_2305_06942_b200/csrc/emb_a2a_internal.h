@@ -30,6 +30,12 @@ struct DevPeers {
   // counter inside peer q's region (rows of our batch block pushed to q)
   float* gstage[kMaxW][2];
   unsigned long long* bflag_out[kMaxW];
+  // buffer-reuse credits: &credits_q[r] / &bcredits_q[r] inside peer q's region.  A rank adds 1
+  // to every peer's slot when a forward (backward) of its starts; a writer stores into peer q's
+  // receive half (gradient staging half) only once q's credit proves q has consumed the previous
+  // contents
+  unsigned long long* credit_out[kMaxW];
+  unsigned long long* bcredit_out[kMaxW];
 };
 
 // Kernel parameters, passed by value (constant bank).  Scalars + the two small tables the
@@ -43,6 +49,7 @@ struct KParams {
   float* send;                  // pool_local staging base ([B][T][D] by global row)
   const DevPeers* peers;
   unsigned long long* flags_in; // own counters, index src * kFlagStride
+  const unsigned long long* credits_in;  // own credit counters (forwards started by src)
   unsigned int* done;           // CTA completion counter (last-CTA detection)
   unsigned int* ticket;         // next chunk ticket (beyond the first gridDim.x)
   unsigned long long* slice_cnt;// per-slice completed-bag counters (monotone over epochs)
@@ -64,7 +71,9 @@ struct KParams {
   int payload_cap;    // rows (TMA) or indices (LSU) a stage holds
   int pdl;            // programmatic dependent launch (overlap with the stream predecessor)
   int rows_wait;      // consumers wait for the predecessor before reading table rows
-  int pdl_trigger;    // trigger the dependent launch at CTA start (else only by exiting)
+  int pdl_trigger;    // trigger the dependent launch once the predecessor is complete (else
+                      // only by exiting)
+  int credit_lag;     // a peer's credit must reach epoch - credit_lag before we store into it
   int flat_below;     // stages whose average bag length is below this use row-flattened pooling
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
@@ -150,6 +159,8 @@ cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counte
                            unsigned long long target, long long timeout_ns, int* err,
                            cudaStream_t st);
 cudaError_t launch_slice_plan(const KParams& P, int* out, cudaStream_t st);
+cudaError_t launch_peer_store_probe(const DevPeers* peers, int W, int r, long long runs,
+                                    cudaStream_t st);
 cudaError_t launch_validate(const int* indices, const int* offsets, long long nnz, long long TB,
                             long long B, int T, const long long* rows_dev, int* err_dev,
                             cudaStream_t st);
@@ -198,6 +209,9 @@ struct PassParams {
   unsigned stamp;              // plan number (30 bits): stale look-back words are ignored
   unsigned long long* trace;   // optional %globaltimer event log (the "trace" option)
   long long trace_cap;
+  int* err;                    // device error word (look-back timeout -> EMB_A2A_ETIMEOUT)
+  long long timeout_ns;
+  int stall;                   // debug: tile 0 publishes a stale stamp (tests the timeout)
 };
 
 // The fused backward (exchange + reduce + update) and the unfused reduce share one kernel.
@@ -206,6 +220,7 @@ struct BwdParams {
   float* stage;                // fused: own staging [B][T][D] for this parity (remote rows)
   const DevPeers* peers;
   unsigned long long* bflags_in;   // own backward arrival counters, src * kFlagStride
+  const unsigned long long* bcredits_in;  // own backward credit counters (backwards started)
   const unsigned* keys;        // sorted plan
   const int* bags;
   const float* wts;            // sorted weights (weighted plan) or NULL

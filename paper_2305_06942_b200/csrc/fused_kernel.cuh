@@ -493,11 +493,11 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
       mbar_init(&empty_bar[i], (unsigned)nconsumer);
     }
   }
-  // Programmatic dependent launch: let the next kernel on the stream start its CTAs (launch ramp,
-  // prologue) as ours retire; it waits at griddepcontrol.wait for us to finish.
-  // (Not when a peer shares this GPU: a rank running ahead would park the waiting CTAs of its
-  // next forwards on SM slots a slower peer's forward needs; exiting triggers it then.)
-  if (P.pdl && P.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Buffer-reuse credit: this forward has started, so everything the caller
+  // ordered before it -- the consumer of our output epoch - 2, which lives in the receive half
+  // the peers are about to overwrite -- is complete.  One add per peer, before any waiting.
+  if (FUSED && P.W > 1 && blockIdx.x == 0 && tid < P.W && tid != P.r)
+    red_release_sys_add(P.peers->credit_out[tid], 1ull);
   for (int i = tid; i < P.T && i < kMaxSmemTables; i += blockDim.x)
     s_tab[i] = reinterpret_cast<const uint4*>(P.tables[i]);
   for (int i = tid; i < P.W; i += blockDim.x) {
@@ -521,10 +521,19 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
   if (warp == 0) {
     // ===================================================================== producer
     bool waited = !P.pdl;
+    // Programmatic dependent launch: the next kernel on the stream may start its CTAs (launch
+    // ramp, prologue, the work before its own wait) once every CTA of ours has triggered.  We
+    // trigger only after OUR wait has returned, i.e. once our predecessor is complete: a kernel
+    // that triggered at entry would let its successor's pre-wait work (rows gathered early, a
+    // stage stored early) overlap its PREDECESSOR -- forward e+2 storing into the receive half
+    // forward e is still writing, or reading table rows a backward is still updating.
+    // (Not when a peer shares this GPU: a rank running ahead would park the waiting CTAs of its
+    // next forwards on SM slots a slower peer's forward needs; exiting triggers it then.)
     auto pdl_wait_once = [&]() {
       if (!waited) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         waited = true;
+        if (P.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       }
     };
     if (TMA) pdl_wait_once();            // the producer gathers table rows itself
@@ -557,6 +566,26 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
       }
       if (lane32 == 0) trace_ev(P, 3, signalled);
       __syncwarp();
+    };
+    // Credit check (a6 precondition): before the first stage of ours that stores into peer s is
+    // published, s must have started its forward epoch - credit_lag.  Chunks
+    // come destination by destination, so a producer checks each destination once.
+    int cred_ok = -1;
+    auto await_credit = [&](int s) {
+      if (lane32 == 0) {
+        const unsigned long long target = P.epoch - (unsigned long long)P.credit_lag;
+        const unsigned long long* f = P.credits_in + (size_t)s * kFlagStride;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(f) < target) {
+          if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
+            atomicExch(P.err, 0x1000 | s);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      __syncwarp();
+      cred_ok = s;
     };
     int ticket = (int)blockIdx.x;
     int k, s, t, i0, nb;
@@ -609,6 +638,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
           h->flag = s_flag[s];
         }
         __syncwarp();
+        if (FUSED && s != P.r && s != cred_ok) await_credit(s);
         const int* ig = P.indices + base;
         if (TMA) {
           // a3: gather4 groups of rows; rows past cnt (padding to a multiple of 4) read row 0
@@ -639,32 +669,6 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
               const float* wg = P.weights + base;
               const unsigned sw = si + 4u * (unsigned)P.payload_cap;
               for (int q = lane32; q < cnt; q += 32) cp_async4(sw + 4u * (unsigned)q, wg + q);
-            }
-          }
-          // This stage is published before the predecessor is known complete (only the first
-          // one is).  If its consumers do not wait either (rows_wait == 0) and it goes to a
-          // peer, the peer must be done with the buffer half it will overwrite -- the output of
-          // our epoch - 2, which the peer consumed before starting its forward epoch - 1.  The
-          // peer's epoch-(epoch-1) slices for us having all arrived proves it started it
-          // (DESIGN.md §5); a peer that sends us nothing gives no such proof: wait instead.
-          if (FUSED && !waited && !P.rows_wait && s != P.r) {
-            const long long nin = P.peers->n_in[s];
-            if (nin == 0) {
-              pdl_wait_once();
-            } else {
-              if (lane32 == 0) {
-                const unsigned long long target = (P.epoch - 1ull) * (unsigned long long)nin;
-                const unsigned long long* f = P.flags_in + (size_t)s * kFlagStride;
-                const unsigned long long t0 = globaltimer();
-                while (ld_acquire_sys(f) < target) {
-                  if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
-                    atomicExch(P.err, 0x100 | s);
-                    break;
-                  }
-                  __nanosleep(64);
-                }
-              }
-              __syncwarp();
             }
           }
           mbar_arrive(&full_bar[st]);

@@ -95,6 +95,8 @@ struct emb_a2a {
   char* region = nullptr;
   size_t region_bytes = 0;
   unsigned long long* flags = nullptr;   // own counters
+  unsigned long long* credits = nullptr; // own forward credit counters (slot q: written by q)
+  unsigned long long* bcredits = nullptr;
   float* recv[2] = {nullptr, nullptr};
   std::vector<void*> opened;             // IPC-opened peer bases
   DevPeers host_peers{};
@@ -133,7 +135,7 @@ struct emb_a2a {
   int64_t kernel_launches = 0;
 
   // backward (f3)
-  int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0;
+  int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0, sort_stall = 0;
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
   unsigned long long* bflags = nullptr;  // own backward arrival counters
@@ -194,7 +196,13 @@ int check_async(emb_a2a* h) {
     const int v = *(volatile int*)h->h_err;
     h->poisoned = true;
     const char* what =
-        (v & 0x800) ? "backward chunk fold timed out on rank %d (code %d, timeout_ms=%lld)"
+        (v & 0x4000) ? "backward sort look-back timed out on rank %d (code %d, timeout_ms=%lld): "
+                       "a radix tile never published its digit counts"
+        : (v & 0x2000) ? "backward credit wait timed out: rank %d waited for rank %d to start its "
+                         "previous backward (timeout_ms=%lld)"
+        : (v & 0x1000) ? "forward credit wait timed out: rank %d waited for rank %d to start the "
+                         "same forward (timeout_ms=%lld)"
+        : (v & 0x800) ? "backward chunk fold timed out on rank %d (code %d, timeout_ms=%lld)"
         : (v & 0x400) ? "backward exchange wait timed out: rank %d never received all gradient "
                         "rows from rank %d (timeout_ms=%lld)"
         : (v & 0x200) ? "device barrier timed out on rank %d (code %d, timeout_ms=%lld)"
@@ -259,6 +267,7 @@ void release_registration(emb_a2a* h) {
   h->d_done = nullptr;
   h->idx_stage_cap = h->off_stage_cap = 0;
   h->flags = nullptr;
+  h->credits = h->bcredits = nullptr;
   h->recv[0] = h->recv[1] = nullptr;
   h->registered = false;
 }
@@ -317,6 +326,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.box4 = h->box4;
   P.peers = h->d_peers;
   P.flags_in = h->flags;
+  P.credits_in = h->credits;
   P.done = h->d_done;
   P.ticket = h->d_done + 1;
   P.err = h->d_err;
@@ -343,6 +353,12 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.pdl = (int)h->pdl;
   P.rows_wait = 1;
   P.pdl_trigger = (h->W > 1 && h->shared_gpu && h->rows_early != 2) ? 0 : 1;
+  // A peer on this very GPU (virtual ranks, test mode) only has to have started the previous
+  // forward: waiting for the same forward could park our persistent grid on SM slots the
+  // peer's kernel needs.  That keeps the weaker contract (a consumer ordered before our next
+  // forward); one GPU per rank gives the full one (output valid until the second following
+  // forward).
+  P.credit_lag = h->shared_gpu ? 1 : 0;
   P.flat_below = (int)h->flat_below;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
@@ -575,10 +591,11 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   h->rows.assign(rows, rows + num_local_tables);
 
   // ---- symmetric region: [forward arrival counters W x 128 B | barrier counter 128 B |
-  //      backward arrival counters W x 128 B | recv0 | recv1 | gstage0 | gstage1], 256-B aligned
-  //      pieces.  gstage (backward, fp32 tables only): [B][T_r][D] float32 gradient rows pushed
-  //      by their data-parallel owners.
-  const size_t flag_bytes = ((size_t)(2 * h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
+  //      backward arrival counters W x 128 B | forward credits W x 128 B | backward credits
+  //      W x 128 B | recv0 | recv1 | gstage0 | gstage1], 256-B aligned pieces.  gstage
+  //      (backward, fp32 tables only): [B][T_r][D] float32 gradient rows pushed by their
+  //      data-parallel owners.  Credits: slot q counts the forwards (backwards) rank q started.
+  const size_t flag_bytes = ((size_t)(4 * h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
   const size_t buf_bytes = ((size_t)h->b * G * dim * 4 + 255) / 256 * 256;
   auto gstage_bytes = [&](int Tq) -> size_t {
     if (table_dtype != EMB_A2A_F32) return 256;
@@ -590,6 +607,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   CUDA_TRY(h, cudaMemset(h->region, 0, h->region_bytes));
   h->flags = (unsigned long long*)h->region;
   h->bflags = h->flags + (size_t)(h->W + 1) * kFlagStride;
+  h->credits = h->flags + (size_t)(2 * h->W + 1) * kFlagStride;
+  h->bcredits = h->flags + (size_t)(3 * h->W + 1) * kFlagStride;
   h->recv[0] = (float*)(h->region + flag_bytes);
   h->recv[1] = (float*)(h->region + flag_bytes + std::max<size_t>(buf_bytes, 256));
   h->gstage[0] = (float*)(h->region + flag_bytes + 2 * std::max<size_t>(buf_bytes, 256));
@@ -650,6 +669,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
     h->host_peers.barrier_out[q] = (unsigned long long*)(base) + (size_t)h->W * kFlagStride;
     h->host_peers.bflag_out[q] =
         (unsigned long long*)(base) + (size_t)(h->W + 1 + h->rank) * kFlagStride;
+    h->host_peers.credit_out[q] =
+        (unsigned long long*)(base) + (size_t)(2 * h->W + 1 + h->rank) * kFlagStride;
+    h->host_peers.bcredit_out[q] =
+        (unsigned long long*)(base) + (size_t)(3 * h->W + 1 + h->rank) * kFlagStride;
     h->host_peers.gstage[q][0] = (float*)(base + fq + 2 * bufq);
     h->host_peers.gstage[q][1] = (float*)(base + fq + 2 * bufq + gstage_bytes(all[q].T));
   }
@@ -879,6 +902,10 @@ int emb_a2a_forward_host_batch(emb_a2a_t* h, int nsteps, const int32_t* const* h
     // one of two steps ago) has been copied out
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_in, 0));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_out[(h->epoch + 1) & 1], 0));
+    // a peer on this same GPU only waits for our previous forward (credit_lag 1): the copy of
+    // the previous step's result must then be out before this forward starts
+    if (h->W > 1 && h->shared_gpu)
+      CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_out[h->epoch & 1], 0));
     float* dout = nullptr;
     rc = emb_a2a_forward(h, h->d_idx_stage[par], h->d_off_stage[par], num_indices[k], stream,
                          &dout, nullptr, nullptr);
@@ -966,6 +993,7 @@ BwdParams bwd_params(emb_a2a* h, const float* grad, float lr, int fused) {
   P.grad = grad;
   P.peers = h->d_peers;
   P.bflags_in = h->bflags;
+  P.bcredits_in = h->bcredits;
   P.keys = h->d_keys[h->plan_buf];
   P.bags = h->d_bags[h->plan_buf];
   P.wts = h->plan_weighted ? h->d_wts[h->plan_buf] : nullptr;
@@ -1160,6 +1188,9 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.stamp = h->plan_no;
     q.trace = h->d_trace;
     q.trace_cap = h->trace_cap;
+    q.err = h->d_err;
+    q.timeout_ns = (long long)h->timeout_ms * 1000000ll;
+    q.stall = (int)h->sort_stall;
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -1227,6 +1258,32 @@ int emb_a2a_device_barrier(emb_a2a_t* h, void* stream) {
                              (long long)h->timeout_ms * 1000000ll, h->d_err,
                              (cudaStream_t)stream));
   h->kernel_launches++;
+  return EMB_A2A_OK;
+}
+
+int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
+                             int64_t* bytes_used) {
+  if (!h || !bytes_used) return EMB_A2A_EINVAL;
+  *bytes_used = 0;
+  int rc = check_async(h);
+  if (rc) return rc;
+  if (!h->registered) return fail(h, EMB_A2A_ESTATE, "peer_store_probe before register_tables");
+  if (bytes_per_peer < 0) return fail(h, EMB_A2A_EINVAL, "bytes_per_peer < 0");
+  if (h->W == 1) return EMB_A2A_OK;
+  // the smallest peer receive region (both halves) bounds what may be written: 512-B runs
+  int64_t cap = -1;
+  for (int q = 0; q < h->W; ++q) {
+    if (q == h->rank) continue;
+    const int64_t bq = h->part[q + 1] - h->part[q];
+    const int64_t half = std::max<int64_t>((bq * h->G * h->D * 4 + 255) / 256 * 256, 256);
+    cap = cap < 0 ? 2 * half : std::min<int64_t>(cap, 2 * half);
+  }
+  const long long runs = std::min<int64_t>(bytes_per_peer, cap) / 512;
+  if (runs <= 0) return EMB_A2A_OK;
+  DeviceGuard guard(h->dev);
+  CUDA_TRY(h, launch_peer_store_probe(h->d_peers, h->W, h->rank, runs, (cudaStream_t)stream));
+  h->kernel_launches++;
+  *bytes_used = (int64_t)runs * 512;
   return EMB_A2A_OK;
 }
 
@@ -1305,7 +1362,8 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2}");
     h->sort_mode = v;
   } else if (k == "bwd_threads") {
-    if (v < 32 || v > 256 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..256, x32");
+    // bwd_kernel is compiled with __launch_bounds__(128, ...): more threads cannot launch
+    if (v < 32 || v > 128 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..128, x32");
     h->bwd_threads = v;
     h->bwd_mode = -1;
   } else if (k == "bwd_share") {
@@ -1314,6 +1372,8 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     h->bwd_mode = -1;
   } else if (k == "debug_delay_ns") {
     h->delay_ns = std::max<int64_t>(0, v);
+  } else if (k == "debug_sort_stall") {
+    h->sort_stall = v ? 1 : 0;
   } else if (k == "debug_skip_signal_to") {
     h->skip_to = v;
   } else {
@@ -1345,6 +1405,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;
+  else if (k == "debug_sort_stall") *v = h->sort_stall;
   else if (k == "debug_skip_signal_to") *v = h->skip_to;
   else return EMB_A2A_EINVAL;
   return EMB_A2A_OK;

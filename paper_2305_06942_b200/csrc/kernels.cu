@@ -25,6 +25,26 @@ __global__ void barrier_kernel(const DevPeers* __restrict__ peers, unsigned long
   }
 }
 
+// NVLink store probe (bench tooling, not the hot path): every CTA streams 16-byte st.global.v4
+// stores -- the fused kernel's store instruction -- into the receive regions of all peers at
+// once, 512-byte runs per warp, consecutive warps on different peers (staggered like row a1).
+// Measures what SM-issued peer stores sustain with every rank sending to every peer.
+__global__ void __launch_bounds__(256) peer_store_probe_kernel(const DevPeers* __restrict__ peers,
+                                                               int W, int r, long long runs) {
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long total = runs * (W - 1);
+  const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < total;
+       c += nwarps) {
+    const int k = (int)(c % (W - 1));
+    const long long run = c / (W - 1);
+    const int q = (r + 1 + k) % W;
+    float* dst = peers->recv[q][0] + run * 128 + lane * 4;
+    st_out4(dst, v);
+  }
+}
+
 __global__ void slice_plan_kernel(const __grid_constant__ KParams P, int* out) {
   const int ticket = blockIdx.x * blockDim.x + threadIdx.x;
   if (ticket >= P.nslices) return;   // slice-level decode (the signal units)
@@ -130,6 +150,15 @@ cudaError_t launch_barrier(const DevPeers* peers, unsigned long long* own_counte
                            cudaStream_t st) {
   barrier_kernel<<<1, ((W + 31) / 32) * 32, 0, st>>>(peers, own_counter, W, r, target, timeout_ns,
                                                      err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_store_probe(const DevPeers* peers, int W, int r, long long runs,
+                                    cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  peer_store_probe_kernel<<<sms * 4, 256, 0, st>>>(peers, W, r, runs);
   return cudaGetLastError();
 }
 

@@ -286,6 +286,15 @@ class EmbA2A:
         self._err(lib.emb_a2a_device_barrier(self._h, _stream_ptr(stream, self.device)),
                   "emb_a2a_device_barrier")
 
+    def peer_store_probe(self, bytes_per_peer: int, stream=None) -> int:
+        """Bench tooling: one kernel storing into every peer's receive region at once (see
+        emb_a2a.h); overwrites the peers' receive buffers.  Returns bytes written per peer."""
+        used = ctypes.c_int64()
+        self._err(lib.emb_a2a_peer_store_probe(self._h, int(bytes_per_peer),
+                                               _stream_ptr(stream, self.device), ctypes.byref(used)),
+                  "emb_a2a_peer_store_probe")
+        return used.value
+
     def destroy(self) -> None:
         if self._h:
             rc = lib.emb_a2a_destroy(self._h)

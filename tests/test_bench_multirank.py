@@ -27,7 +27,7 @@ def test_bench_torchrun_shared_gpu(n):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "4", "--warmup", "3",
-           "--config", "tiny", "--batches", "2", "--no-cpu"]
+           "--config", "tiny", "--batches", "2", "--cpu-seconds", "1"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -38,3 +38,12 @@ def test_bench_torchrun_shared_gpu(n):
     assert line["gpu_launches"] == 4
     bwd = line["backward"]          # f3 across processes: fused exchange vs pack + all_to_all
     assert bwd["fused_equals_unfused_bitwise"] is True and bwd["us_per_step"] > 0
+    par = line["parity"]            # every rank checked its own rows against the oracle
+    assert par["within_tol"] is True and par["bitwise"] is True and par["rows"] >= 16
+    cpu = line["cpu_baseline"]      # N single-threaded oracle processes, one per rank
+    assert cpu["cores"] == n and len(cpu["per_rank"]) == n and cpu["value"] > 0
+    assert cpu["host_cpu_count"] >= 1
+    roof = line["roofline"]
+    assert roof["compulsory_bytes_per_launch"] <= roof["algorithmic_bytes_per_launch"]
+    assert 0 < roof["frac_compulsory"] <= roof["frac"]
+    assert line["alpha0"]["us_per_step"] > 0
