@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--vec", type=int, default=0)
     ap.add_argument("--order", type=int, default=-1)
+    ap.add_argument("--ctas-per-sm", type=int, default=0, help="persistent grid per SM (E3)")
+    ap.add_argument("--skew-us", type=float, default=0.0,
+                    help="E5: the last rank sleeps this long on the GPU before each forward")
     ap.add_argument("--batches", type=int, default=16,
                     help="distinct pre-generated batches rotated through the timed steps")
     ap.add_argument("--timing", default="b2b", choices=["b2b", "flushed"],
@@ -149,6 +152,37 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+class NvlinkCounters:
+    """This GPU's NVLink data-TX byte counter through NVML field values (summed over links) --
+    the non-profiler evidence of NVLink traffic (ncu cannot wrap the multi-rank run: its
+    serialised replay deadlocks the receive wait).  None where NVML has no such counter."""
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.ok = self.read() is not None
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        try:
+            nv = self.nv
+            fid = nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [(fid, link) for link in range(18)])
+            tot, seen = 0, False
+            for v in vals:
+                if getattr(v, "nvmlReturn", 1) == 0:
+                    tot += int(v.value.ullVal)
+                    seen = True
+            return tot * 1024 if seen else None
+        except Exception:
+            return None
 
 
 # ---------------------------------------------------------------------------- oracle timing
@@ -333,6 +367,8 @@ def main():
         h.set_option("vec", args.vec)
     if args.order >= 0:
         h.set_option("order", args.order)
+    if args.ctas_per_sm:
+        h.set_option("ctas_per_sm", args.ctas_per_sm)
     h.register_tables(tables, cfg.B, pooling=args.pooling)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -385,13 +421,21 @@ def main():
         return float(t.item())
 
     # ---- fused (the product)
-    fused_step = lambda k: h.forward(d_in[k][0], d_in[k][1], stream,  # noqa: E731
-                                     per_sample_weights=None if d_w is None else d_w[k])
+    skew_cycles = int(args.skew_us * 1965) if (args.skew_us > 0 and rank == N - 1) else 0
+
+    def fused_step(k):
+        if skew_cycles:                   # E5: a late rank (its peers wait for its slices)
+            torch.cuda._sleep(skew_cycles)
+        return h.forward(d_in[k][0], d_in[k][1], stream,
+                         per_sample_weights=None if d_w is None else d_w[k])
     launches0 = h.query("kernel_launches")
     clk = ClockSampler(local)
+    nvc = NvlinkCounters(local) if (N > 1 and not shared) else None
+    tx0 = nvc.read() if nvc else None
     clk.start()
     b2b_ms = b2b_loop(fused_step, args.steps, args.warmup)
     clocks = clk.stop()
+    tx1 = nvc.read() if nvc else None
     launches = h.query("kernel_launches") - launches0 - args.warmup
     launches -= 1 if N > 1 else 0          # the device barrier before the timed region
     ms = timed_loop(fused_step, args.steps, args.warmup)     # flushed, per-step events
@@ -464,7 +508,14 @@ def main():
                             peak_hbm, esize)
     nvl = None
     if N > 1 and not shared:
-        nvl = nvlink_probe(h, N, stream, max_over_ranks)
+        nvl = nvlink_probe(h, N, stream, max_over_ranks) or {}
+        if tx0 is not None and tx1 is not None:
+            steps_in = args.steps + args.warmup     # the counters saw warm-up steps too
+            nvl["nvml_tx_bytes_per_step"] = (tx1 - tx0) / steps_in
+            nvl["algorithmic_tx_bytes_per_step"] = tx_b
+            nvl["nvml_tx_gbs_during_b2b"] = (tx1 - tx0) / steps_in * args.steps / (b2b_ms / 1e3) / 1e9
+            nvl["nvml_note"] = ("NVML NVLink data-TX counters (KiB granularity, all links) "
+                                "around the warm-up + timed back-to-back loop, this rank")
         if nvl and nvl.get("tx_gbs_per_gpu") and roof["bound"] == "nvlink":
             roof["peak_measured_probe"] = nvl["tx_gbs_per_gpu"]
             roof["frac_vs_probe"] = roof["achieved"] / nvl["tx_gbs_per_gpu"]
@@ -568,6 +619,8 @@ def main():
                    "per_sample_weights": bool(args.weighted),
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
+                   "order": h.get_option("order"), "ctas_per_sm": h.get_option("ctas_per_sm"),
+                   "skew_us_last_rank": args.skew_us,
                    "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
                           "distinct rows) over %.1f GB of tables, K back-to-back steps" %
                           (args.batches, args.batches * working_set_mb(cfg, mine[0][0], mine[0][1]),

@@ -47,3 +47,22 @@ def test_bench_torchrun_shared_gpu(n):
     assert roof["compulsory_bytes_per_launch"] <= roof["algorithmic_bytes_per_launch"]
     assert 0 < roof["frac_compulsory"] <= roof["frac"]
     assert line["alpha0"]["us_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_ablations_command_torchrun_shared_gpu():
+    """f1 as one driver-runnable command (tools/ablations_torchrun.py): every point is a torchrun
+    bench run that prints a JSON line with its ablation key, parity-checked."""
+    env = dict(os.environ, EMBA2A_SHARED_GPU="1")
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "ablations_torchrun.py"), "--gpus", "2",
+           "--config", "tiny", "--slices", "4,32", "--ctas", "1", "--steps", "3", "--warmup", "3",
+           "--batches", "2", "--skew-us", "5"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    recs = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(recs) == 2 + 1 + 6, r.stdout[-2000:]
+    for rec in recs:
+        assert "error" not in rec, rec
+        assert rec["us_per_step"] > 0 and rec["parity"]["within_tol"] is True
+    kinds = [next(iter(rec["ablation"])) for rec in recs]
+    assert kinds == ["E4", "E4", "E3"] + ["E5"] * 6
