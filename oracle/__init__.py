@@ -72,6 +72,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_bf16_to_float.argtypes = [ctypes.c_uint16]
         L.oracle_f16_to_float.restype = ctypes.c_float
         L.oracle_f16_to_float.argtypes = [ctypes.c_uint16]
+        L.oracle_round_to_half.restype = ctypes.c_uint16
+        L.oracle_round_to_half.argtypes = [ctypes.c_float, I32]
+        L.oracle_round_array.restype = None
+        L.oracle_round_array.argtypes = [P, P, I64, I32]
         L.oracle_backward_sgd.restype = I32
         L.oracle_backward_sgd.argtypes = [I32, P, I32, I64, P, P, P, P, P, P, P, I32, P,
                                           ctypes.c_float]
@@ -125,6 +129,16 @@ F32, BF16, F16 = 0, 1, 2
 SUM, MEAN = 0, 1
 
 
+def round_to_half(a: np.ndarray, dtype: int) -> np.ndarray:
+    """16-bit output (R#32): float32 values -> bfloat16 (BF16) or binary16 (F16) bits, rounded
+    to nearest, ties to even, once (oracle.c oracle_round_to_half)."""
+    x = np.ascontiguousarray(a, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.uint16)
+    if x.size:
+        lib().oracle_round_array(_ptr(x), _ptr(out), x.size, dtype)
+    return out
+
+
 def bf16_to_float(bits: int) -> float:
     return float(lib().oracle_bf16_to_float(bits))
 
@@ -145,12 +159,14 @@ def _weights(weights, idx):
 def emb_a2a(part: Sequence[int], D: int, B: int, T: Sequence[int], tables: Sequence[np.ndarray],
             indices: Sequence[np.ndarray], offsets: Sequence[np.ndarray],
             precision: int = 32, dtype: int = F32, weights: Optional[Sequence[np.ndarray]] = None,
-            pooling: int = SUM) -> List[np.ndarray]:
+            pooling: int = SUM, out_dtype: int = F32) -> List[np.ndarray]:
     """The plain definition over materialised tables (G arrays [rows_g, D]).
 
     dtype F32: float32 tables; BF16 / F16: uint16 arrays holding bfloat16 / binary16 bits.
     weights: optional per-rank per-sample weights aligned with indices (sum pooling only).
     pooling: SUM or MEAN (P:119 ..._sum_mean).
+    out_dtype: F32, or BF16 / F16 for a 16-bit output: the fp32 result rounded once, to nearest
+    even (R#32) -- returned as uint16 bit arrays.
     Returns out_s for every destination rank s: [b_s, G*D], float32 (precision=32) or float64.
     """
     W = len(T)
@@ -171,14 +187,19 @@ def emb_a2a(part: Sequence[int], D: int, B: int, T: Sequence[int], tables: Seque
                                  precision, _ptr(keep[3]))
     if rc:
         raise OracleError(rc, "emb_a2a")
+    if out_dtype != F32:
+        assert precision == 32
+        return [round_to_half(o, out_dtype) for o in outs]
     return outs
 
 
 def emb_a2a_rows(seed: int, mode: int, part: Sequence[int], D: int, B: int, T: Sequence[int],
                  R: int, indices: Sequence[np.ndarray], offsets: Sequence[np.ndarray], s: int,
                  rows_i: Sequence[int], precision: int = 32, check_inputs: bool = True,
-                 weights: Optional[Sequence[np.ndarray]] = None, pooling: int = SUM) -> np.ndarray:
-    """Selected rows of out_s with procedural tables (every table has R rows)."""
+                 weights: Optional[Sequence[np.ndarray]] = None, pooling: int = SUM,
+                 out_dtype: int = F32) -> np.ndarray:
+    """Selected rows of out_s with procedural tables (every table has R rows); out_dtype as in
+    emb_a2a (16-bit outputs come back as uint16 bits)."""
     W = len(T)
     p, Ta, idx, off, nnz = _common(part, T, indices, offsets)
     G = int(Ta.sum())
@@ -195,6 +216,9 @@ def emb_a2a_rows(seed: int, mode: int, part: Sequence[int], D: int, B: int, T: S
                                       int(check_inputs))
     if rc:
         raise OracleError(rc, "emb_a2a_rows")
+    if out_dtype != F32:
+        assert precision == 32
+        return round_to_half(out[: sel.size], out_dtype)
     return out[: sel.size]
 
 

@@ -34,6 +34,9 @@
  *   oracle_table_value      pinned: closed-form value ranges / grid, splitmix64 published vectors
  *   oracle_slice_plan       pinned: P:145-147 example (B=4, N=2, S=2 -> 2 slices/table),
  *                           S:144 clipping example (S=3, b=4 -> 3,1), partition invariant
+ *   oracle_round_to_half    pinned: numpy float32 -> float16 and torch float32 -> bfloat16
+ *                           (both round-to-nearest-even) on every 16-bit high half x boundary /
+ *                           tie / random low halves, hand-worked ties, overflow, subnormals
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -122,6 +125,55 @@ float oracle_f16_to_float(uint16_t h) {
     float f;
     memcpy(&f, &u, 4);
     return f;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * 16-bit output (f2, SURVEY 8(f) item 2 "fp16 output to halve NVLink bytes"; reading R#32):
+ * the pooled value is the fp32 result above, then rounded ONCE to the output type, to nearest,
+ * ties to even (IEEE 754 roundTiesToEven).  Written from that definition: over the positive
+ * patterns 0 .. +inf the values of a 16-bit float grow with the bit pattern, so the two
+ * candidates bracketing |v| are found by bisection over the patterns; the nearer one wins, a
+ * tie goes to the even pattern (last mantissa bit 0).  +inf stands in as the next value after
+ * the largest finite one with its unbounded-exponent value (2^128 for bfloat16, 2^16 for
+ * binary16), which is IEEE's overflow rule for roundTiesToEven.  The sign is copied (-0 -> -0).
+ * NaN -> the quiet NaN of the type (never produced by finite tables).
+ * ---------------------------------------------------------------------------------------- */
+static double half_pattern_value(uint16_t h, int dtype) {   /* positive patterns only */
+    if (dtype == ORACLE_BF16) {
+        if (h == 0x7F80) return 340282366920938463463374607431768211456.0;   /* 2^128 */
+        return (double)oracle_bf16_to_float(h);
+    }
+    if (h == 0x7C00) return 65536.0;                                           /* 2^16 */
+    return (double)oracle_f16_to_float(h);
+}
+
+uint16_t oracle_round_to_half(float v, int dtype) {
+    const uint16_t inf = dtype == ORACLE_BF16 ? 0x7F80 : 0x7C00;
+    const uint16_t qnan = dtype == ORACLE_BF16 ? 0x7FC0 : 0x7E00;
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    const uint16_t sign = (uint16_t)((u >> 31) << 15);
+    if (v != v) return (uint16_t)(sign | qnan);
+    const double a = v < 0 ? -(double)v : (double)v;       /* exact */
+    if (a >= half_pattern_value(inf, dtype)) return (uint16_t)(sign | inf);
+    /* largest positive pattern lo with value(lo) <= a (lo < inf) */
+    uint16_t lo = 0, hi = inf;                               /* value(lo) <= a < value(hi) */
+    while (hi - lo > 1) {
+        const uint16_t mid = (uint16_t)(lo + (hi - lo) / 2);
+        if (half_pattern_value(mid, dtype) <= a) lo = mid; else hi = mid;
+    }
+    const double dlo = a - half_pattern_value(lo, dtype);
+    const double dhi = half_pattern_value(hi, dtype) - a;
+    uint16_t r;
+    if (dlo < dhi) r = lo;
+    else if (dhi < dlo) r = hi;
+    else r = (lo & 1) ? hi : lo;                             /* tie: even pattern */
+    return (uint16_t)(sign | r);
+}
+
+/* Element-wise over an array (the oracle's fp32 output -> 16-bit output bits). */
+void oracle_round_array(const float* in, uint16_t* out, int64_t n, int dtype) {
+    for (int64_t k = 0; k < n; ++k) out[k] = oracle_round_to_half(in[k], dtype);
 }
 
 static float table_at(const tables_t* tb, int64_t g, int64_t row, int64_t d) {

@@ -168,3 +168,83 @@ def test_procedural_rows_ex_equal_materialised():
                                        [c[0] for c in csr], [c[1] for c in csr], s, np.arange(b),
                                        weights=ww, pooling=pooling)
             np.testing.assert_array_equal(rows, full[s])
+
+
+# ------------------------------------------------------------------ 16-bit output (R#32)
+
+def _sweep_f32_patterns(seed=0):
+    """Every 16-bit high half x low halves that sit on and around both types' rounding
+    boundaries (bf16 ties at 0x8000, binary16 ties at bit 12 in the normal range and higher
+    bits for subnormals), plus random patterns; NaN patterns dropped."""
+    hi = np.arange(1 << 16, dtype=np.uint32) << np.uint32(16)
+    lows = np.array([0x0000, 0x0001, 0x0FFF, 0x1000, 0x1001, 0x1FFF, 0x2000, 0x3000, 0x7FFF,
+                     0x8000, 0x8001, 0xBFFF, 0xC000, 0xFFFF], dtype=np.uint32)
+    pats = (hi[:, None] | lows[None, :]).ravel()
+    rng = np.random.default_rng(seed)
+    pats = np.concatenate([pats, rng.integers(0, 1 << 32, 400_000, dtype=np.uint64).astype(np.uint32)])
+    f = pats.view(np.float32)
+    return f[~np.isnan(f)]
+
+
+def test_round_to_half_f16_equals_numpy():
+    """Pin: numpy's float32 -> float16 cast rounds to nearest even (incl. subnormals, overflow
+    to inf); the oracle's bisection over the binary16 patterns must agree on every pattern."""
+    f = _sweep_f32_patterns(1)
+    with np.errstate(over="ignore"):
+        want = f.astype(np.float16).view(np.uint16)
+    np.testing.assert_array_equal(oracle.round_to_half(f, oracle.F16), want)
+
+
+def test_round_to_half_bf16_equals_torch():
+    """Pin: torch's float32 -> bfloat16 conversion rounds to nearest even."""
+    f = _sweep_f32_patterns(2)
+    want = torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(oracle.round_to_half(f, oracle.BF16), want)
+
+
+@pytest.mark.parametrize("v,dt,bits", [
+    (1.0 + 2.0 ** -8, oracle.BF16, 0x3F80),        # tie 1.0 | 1+2^-7 -> even (1.0)
+    (1.0 + 3 * 2.0 ** -8, oracle.BF16, 0x3F82),    # tie 1+2^-7 | 1+2^-6 -> even
+    (-(1.0 + 2.0 ** -9), oracle.BF16, 0xBF80),     # below half an ulp -> down, sign kept
+    (65520.0, oracle.F16, 0x7C00),                 # tie 65504 (odd) | 2^16 -> inf (IEEE)
+    (65519.0, oracle.F16, 0x7BFF),                 # below the tie: largest finite
+    (2.0 ** -25, oracle.F16, 0x0000),              # tie 0 | smallest subnormal -> 0 (even)
+    (3 * 2.0 ** -26, oracle.F16, 0x0001),          # 0.75 of the smallest subnormal -> up
+    (-0.0, oracle.F16, 0x8000), (-0.0, oracle.BF16, 0x8000),
+    (1.0 + 2.0 ** -11, oracle.F16, 0x3C00),        # tie 1.0 | 1+2^-10 -> even
+    (2049.0, oracle.F16, 0x6800),                  # tie 2048 | 2050 -> 2048 (even)
+])
+def test_round_to_half_worked_cases(v, dt, bits):
+    assert int(oracle.round_to_half(np.array([v], np.float32), dt)[0]) == bits
+
+
+def test_half_output_is_the_rounded_fp32_result():
+    """out_dtype = BF16 / F16: the fp32 definition rounded once.  On exact-int tables the sums
+    are integers of magnitude < 2^11, exact in binary16 (and in bf16 below 2^8): the bits are
+    then those of the exact integer sum (closed form, independent of the rounding code)."""
+    rng = np.random.default_rng(77)
+    W, T, B, D, R = 2, [2, 3], 8, 8, 11
+    tables = [rng.integers(-8, 8, size=(R, D)).astype(np.float32) for _ in range(5)]
+    idx, off = [], []
+    for r in range(W):
+        i, o = csr_from_bags([[list(rng.integers(0, R, size=rng.integers(0, 9))) for _ in range(B)]
+                              for _ in range(T[r])])
+        idx.append(i)
+        off.append(o)
+    part = synth.even_partition(B, W)
+    f32 = oracle.emb_a2a(part, D, B, T, tables, idx, off)
+    for dt in (oracle.F16, oracle.BF16):
+        got = oracle.emb_a2a(part, D, B, T, tables, idx, off, out_dtype=dt)
+        for s in range(W):
+            assert got[s].dtype == np.uint16
+            np.testing.assert_array_equal(got[s], oracle.round_to_half(f32[s], dt))
+            if dt == oracle.F16:
+                np.testing.assert_array_equal(got[s], f32[s].astype(np.float16).view(np.uint16))
+            small = np.abs(f32[s]) < 256
+            bf = torch.from_numpy(f32[s]).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+            if dt == oracle.BF16:
+                np.testing.assert_array_equal(got[s][small], bf[small])
+        rows = oracle.emb_a2a_rows(5, 1, part, D, B, T, R, idx, off, 1, np.arange(B // W),
+                                   out_dtype=dt)
+        full = oracle.emb_a2a_rows(5, 1, part, D, B, T, R, idx, off, 1, np.arange(B // W))
+        np.testing.assert_array_equal(rows, oracle.round_to_half(full, dt))
