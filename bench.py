@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--table-dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="table element type (f2; fp32 accumulation and output either way)")
     ap.add_argument("--pooling", default="sum", choices=["sum", "mean"], help="f2: mean pooling")
+    ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16", "f16"],
+                    help="f2: output element type (fp32 sum rounded once, R#32; halves TX bytes)")
     ap.add_argument("--weighted", action="store_true", help="f2: per-sample weights")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-alpha0", action="store_true",
@@ -90,15 +92,15 @@ def workload_desc(cfg):
             f"global batch {cfg.B}, {pool}, Zipf alpha={cfg.alpha}, fp32")
 
 
-def algorithmic_bytes(cfg, r, nnz, esize=4, weighted=False):
+def algorithmic_bytes(cfg, r, nnz, esize=4, weighted=False, oes=4):
     """Per-rank algorithmic bytes of one forward: gathered rows (esize bytes
     per element) + indices (+ weights) + offsets + this rank's receive buffer; and the bytes it
     must send over NVLink."""
     b = int(cfg.part[r + 1] - cfg.part[r])
     T = cfg.T[r]
     hbm = nnz * cfg.D * esize + nnz * (8 if weighted else 4) + (T * cfg.B + 1) * 4 + \
-        b * cfg.G * cfg.D * 4
-    tx = (cfg.B - b) * T * cfg.D * 4
+        b * cfg.G * cfg.D * oes
+    tx = (cfg.B - b) * T * cfg.D * oes
     return hbm, tx
 
 
@@ -369,6 +371,10 @@ def main():
         h.set_option("order", args.order)
     if args.ctas_per_sm:
         h.set_option("ctas_per_sm", args.ctas_per_sm)
+    ODT = {"f32": 0, "bf16": 1, "f16": 2}[args.out_dtype]
+    oes = 4 if ODT == 0 else 2
+    if ODT:
+        h.set_option("out_dtype", ODT)
     h.register_tables(tables, cfg.B, pooling=args.pooling)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -450,7 +456,7 @@ def main():
     # events over the timed region
     nnz_mean = float(np.mean([mine[k % args.batches][0].size for k in range(args.steps)]))
     hbm_b, tx_b = algorithmic_bytes(cfg, rank, nnz_mean, 4 if args.table_dtype == "f32" else 2,
-                                    args.weighted)
+                                    args.weighted, oes)
     peak_hbm, peak_src = measured_peaks()
     t_hbm = hbm_b / (peak_hbm * 1e9)
     t_nvl = tx_b / (NVLINK_GBS * 1e9)
@@ -492,7 +498,7 @@ def main():
     # ---- the same step against compulsory bytes and DRAM traffic, and the alpha = 0 control
     esize = 4 if args.table_dtype == "f32" else 2
     comp_b = float(np.mean([compulsory_bytes(cfg, rank, mine[k % args.batches][0],
-                                             mine[k % args.batches][1], esize, args.weighted)
+                                             mine[k % args.batches][1], esize, args.weighted, oes)
                             for k in range(min(args.steps, args.batches))]))
     kern_s = ms_step / 1e3
     roof["compulsory_bytes_per_launch"] = comp_b
@@ -505,7 +511,7 @@ def main():
     alpha0 = None
     if not args.no_alpha0 and args.alpha != 0.0:
         alpha0 = alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks,
-                            peak_hbm, esize)
+                            peak_hbm, esize, oes)
     nvl = None
     if N > 1 and not shared:
         nvl = nvlink_probe(h, N, stream, max_over_ranks) or {}
@@ -522,7 +528,7 @@ def main():
 
     # ---- end to end through the public API: pinned host inputs -> device -> host result
     b = h.b
-    h_out = torch.empty((b, h.G * h.D), dtype=torch.float32).pin_memory()
+    h_out = torch.empty((b, h.G * h.D), dtype=h.out_dtype).pin_memory()
     # the pipelined serving loop (emb_a2a_forward_host_batch): every step copies its inputs in
     # and its result out; neighbouring steps' copies overlap the forwards
     h_outs = [h_out, torch.empty_like(h_out).pin_memory()]
@@ -545,7 +551,7 @@ def main():
     h2d = float(np.mean([(mine[k % args.batches][0].size + mine[k % args.batches][1].size) * 4
                          for k in range(args.steps)]))
     e2e = {"value": lookups / (e2e_total / 1e3), "unit": "lookups/s",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(b * h.G * h.D * 4),
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(b * h.G * h.D * oes),
            "ms_per_step": e2e_total / args.steps,
            "api": "emb_a2a_forward_host_batch (pinned host in/out, copies overlapped across steps)"}
     if args.weighted:
@@ -555,9 +561,9 @@ def main():
     unfused = None
     if not args.no_baseline:
         T = cfg.T[rank]
-        send = torch.empty((cfg.B, T, cfg.D), dtype=torch.float32, device=dev)
-        recv = torch.empty((N, b, T, cfg.D), dtype=torch.float32, device=dev)
-        final = torch.empty((b, cfg.G * cfg.D), dtype=torch.float32, device=dev)
+        send = torch.empty((cfg.B, T, cfg.D), dtype=h.out_dtype, device=dev)
+        recv = torch.empty((N, b, T, cfg.D), dtype=h.out_dtype, device=dev)
+        final = torch.empty((b, cfg.G * cfg.D), dtype=h.out_dtype, device=dev)
 
         def unfused_step(k, permute):
             h.pool_local(d_in[k][0], d_in[k][1], send, stream,
@@ -610,12 +616,14 @@ def main():
         "value": value, "unit": "lookups/s", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "us_per_step": ms_step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.table_dtype == "f32" else f"{args.table_dtype}-tables/f32-accumulate",
+        "dtype": ("f32" if args.table_dtype == "f32" else f"{args.table_dtype}-tables/f32-accumulate")
+                 + ("" if ODT == 0 else f"/{args.out_dtype}-output"),
         "data": "synthetic (seeded Zipf indices, procedural fp32 tables; DESIGN.md Input recipe)",
         "config": {"workload": workload_desc(cfg), "global_batch": cfg.B,
                    "tables_per_rank": cfg.T[0], "rows": cfg.R, "dim": cfg.D,
                    "pooling": list(cfg.pool), "alpha": cfg.alpha, "world": N,
                    "table_dtype": args.table_dtype, "pooling_mode": args.pooling,
+                   "out_dtype": args.out_dtype,
                    "per_sample_weights": bool(args.weighted),
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
@@ -763,32 +771,44 @@ def parity_check(args, cfg, h, csr_all, w_all, rank, dev, stream, d_in0, d_w0, n
     while sel.size < min(nsample, b):
         sel = np.unique(np.concatenate([sel, rng.integers(0, b, nsample)]))[:min(nsample, b)]
     t0 = time.perf_counter()
+    odt = {torch.float32: oracle.F32, torch.bfloat16: oracle.BF16, torch.float16: oracle.F16}[h.out_dtype]
     ref = oracle.emb_a2a_rows(cfg.table_seed, cfg.value_mode, cfg.part, cfg.D, cfg.B, cfg.T, cfg.R,
                               [c[0] for c in csr_all], [c[1] for c in csr_all], rank, sel,
                               check_inputs=False, weights=w_all,
-                              pooling=oracle.MEAN if args.pooling == "mean" else oracle.SUM)
+                              pooling=oracle.MEAN if args.pooling == "mean" else oracle.SUM,
+                              out_dtype=odt)
     secs = time.perf_counter() - t0
-    got = out[torch.from_numpy(sel).to(dev)].cpu().numpy()
+    got_t = out[torch.from_numpy(sel).to(dev)]
+    if odt == oracle.F32:
+        got = got_t.cpu().numpy()
+        bitwise = bool(np.array_equal(got.view(np.uint32), ref.view(np.uint32)))
+        tol = 1e-6 + 1e-5 * np.abs(ref.astype(np.float64))
+    else:   # 16-bit output: the rounded oracle value, bit for bit (R#32)
+        bits = got_t.view(torch.int16).cpu().numpy().view(np.uint16)
+        bitwise = bool(np.array_equal(bits, ref))
+        got = got_t.float().cpu().numpy()
+        ref = torch.from_numpy(ref.view(np.int16)).view(h.out_dtype).float().numpy()
+        tol = np.zeros(ref.shape)
     err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
-    tol = 1e-6 + 1e-5 * np.abs(ref.astype(np.float64))
     return {"rows": int(sel.size), "cols": int(ref.shape[1]), "max_abs_err": float(err.max()),
-            "bitwise": bool(np.array_equal(got.view(np.uint32), ref.view(np.uint32))),
-            "within_tol": bool((err <= tol).all()), "oracle_seconds": secs,
+            "bitwise": bitwise, "within_tol": bool((err <= tol).all()) and (odt == oracle.F32 or bitwise),
+            "oracle_seconds": secs,
             "what": "fresh fused forward of batch 0; sampled rows of this rank's output vs "
                     "oracle.emb_a2a_rows (every rank checks its own; the line shows rank 0's)"}
 
 
-def compulsory_bytes(cfg, r, idx, off, esize=4, weighted=False):
+def compulsory_bytes(cfg, r, idx, off, esize=4, weighted=False, oes=4):
     """Bytes one forward cannot avoid moving: each DISTINCT (table, row) once + indices (+
     weights) + offsets + this rank's receive buffer (SURVEY 8(d) "Zipf caveat")."""
     T = cfg.T[r]
     b = int(cfg.part[r + 1] - cfg.part[r])
     uniq = sum(np.unique(idx[off[t * cfg.B]:off[(t + 1) * cfg.B]]).size for t in range(T))
     return uniq * cfg.D * esize + idx.size * (8 if weighted else 4) + (T * cfg.B + 1) * 4 + \
-        b * cfg.G * cfg.D * 4
+        b * cfg.G * cfg.D * oes
 
 
-def alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks, peak_hbm, esize):
+def alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks, peak_hbm, esize,
+               oes=4):
     """The same fused step on uniform indices (alpha = 0: no Zipf reuse, the cold-cache control
     of SURVEY 8(d)), args.alpha0_batches rotating batches, timed like the headline."""
     import torch
@@ -801,8 +821,8 @@ def alpha0_leg(args, cfg, h, rank, N, dev, stream, b2b_loop, max_over_ranks, pea
     step = lambda k: h.forward(d0[k % nb][0], d0[k % nb][1], stream)  # noqa: E731
     ms = max_over_ranks(b2b_loop(step, args.steps, args.warmup)) / args.steps
     nnz = float(np.mean([mine0[k % nb][0].size for k in range(args.steps)]))
-    hbm_b, _ = algorithmic_bytes(cfg0, rank, nnz, esize, False)
-    comp = float(np.mean([compulsory_bytes(cfg0, rank, i, o, esize) for i, o in mine0]))
+    hbm_b, _ = algorithmic_bytes(cfg0, rank, nnz, esize, False, oes)
+    comp = float(np.mean([compulsory_bytes(cfg0, rank, i, o, esize, False, oes) for i, o in mine0]))
     del d0
     return {"us_per_step": ms * 1e3, "frac": hbm_b / (ms / 1e3) / 1e9 / peak_hbm,
             "frac_compulsory": comp / (ms / 1e3) / 1e9 / peak_hbm,

@@ -102,8 +102,10 @@ int emb_a2a_register_tables_ex(emb_a2a_t* h, int num_local_tables, const void* c
  *            are local row ids (0 <= idx < rows[t]).  Borrowed until the stream passes the op.
  *  offsets   DEVICE int32[T_r * B + 1]: absolute CSR offsets, offsets[0] = 0, non-decreasing,
  *            offsets[T_r*B] = num_indices (bag (t, j) = indices[offsets[t*B+j] .. offsets[t*B+j+1])).
- *  out       receives a DEVICE pointer to this rank's output [b_r][G*D] float32 row-major, the
- *            layout the interaction op consumes.  Library-owned; valid until the SECOND
+ *  out       receives a DEVICE pointer to this rank's output [b_r][G*D] row-major, the layout
+ *            the interaction op consumes; float32, or -- with set_option("out_dtype")
+ *            -- bfloat16 / binary16 elements (the fp32 sum rounded once to nearest even, R#32),
+ *            which halves the bytes every peer store moves over NVLink.  Library-owned; valid until the SECOND
  *            following forward on this handle or destroy (double buffer by epoch parity).
  *  out_rows, out_cols  receive b_r and G*D (either may be NULL).
  * Preconditions (fast path, unchecked unless set_option("validate",1)): indices in range,
@@ -125,7 +127,7 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
 
 /* The same forward fed from HOST memory (the end-to-end path): copies h_indices / h_offsets
  * (host, ideally pinned) into library-owned device staging, runs the fused forward, and copies
- * the [b_r][G*D] float32 result into h_out (host, b_r*G*D floats).  The forward and the result
+ * the [b_r][G*D] result into h_out (host, b_r*G*D elements of the output type).  The forward and the result
  * copy are enqueued on `stream`; the input copy runs on a library-owned copy stream that
  * `stream` waits for, into one of two staging buffers, so consecutive calls overlap the next
  * call's host->device copy with this call's device->host copy.  Returns after enqueuing;
@@ -136,7 +138,7 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
 /* A sequence of nsteps host-buffer forwards, pipelined (collective; every rank passes the same
  * nsteps): step k copies h_indices[k] (num_indices[k] int32) and h_offsets[k] (T_r*B+1 int32)
  * in on one library copy stream, runs the fused forward on `stream`, and copies the result into
- * h_out[k] (b_r*G*D float32) on a second copy stream -- so step k's result copy overlaps step
+ * h_out[k] (b_r*G*D elements of the output type) on a second copy stream -- so step k's result copy overlaps step
  * k+1's forward and step k+2's input copy (the serving loop).  All host buffers ideally pinned,
  * and left untouched until `stream` is synchronised; `stream` completes only after the last
  * result copy.  Returns after enqueuing. */
@@ -145,8 +147,8 @@ int emb_a2a_forward_host_batch(emb_a2a_t* h, int nsteps, const int32_t* const* h
                                float* const* h_out, void* stream);
 
 /* Unfused baseline, first half (not collective): the same pooling, written with local stores to
- * a caller-owned DEVICE staging buffer `send`, dest-major [W][b_s][T_r][D] float32 (the block of
- * destination s starts at p_s*T_r*D floats).  The second half is the caller's NCCL
+ * a caller-owned DEVICE staging buffer `send`, dest-major [W][b_s][T_r][D] elements of the output
+ * type (the block of destination s starts at p_s*T_r*D elements).  The second half is the caller's NCCL
  * all_to_all_single (P:250 baseline: embedding kernels + RCCL All-to-All). */
 int emb_a2a_pool_local(emb_a2a_t* h, const int32_t* indices, const int32_t* offsets,
                        int64_t num_indices, void* stream, float* send);
@@ -221,6 +223,9 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *   "slice"        S, pooled vectors per slice, >= 1 (P:147 user parameter; default 32)
  *   "order"        0 comm-aware staggered (default), 1 comm-aware ascending, 2 oblivious
  *                  (set before register_tables)
+ *   "out_dtype"    output element type (emb_a2a_dtype): 0 fp32 (default), 1 bf16, 2 fp16 --
+ *                  accumulation stays fp32, the result is rounded once (R#32); identical on all
+ *                  ranks, set before register_tables (the receive buffers are sized for it)
  *   "chunk"        bags per work ticket, 1..63 (default 32; the largest divisor of S not above
  *                  it is used): load-balance granularity, independent of the signal slice S
  *                  (set before register_tables)

@@ -64,6 +64,8 @@ struct KParams {
   int DU;             // 16-byte units per table row (D * element size / 16)
   int elem;           // table element type: 0 fp32, 1 bf16, 2 fp16
   int mean;           // 1: mean pooling (P:119 sum_mean), 0: sum
+  int out_dtype;      // output element type: 0 fp32, 1 bf16, 2 fp16 (R#32: rounded once, RNE)
+  int oshift;         // log2 of the output element size (2 or 1)
   int tma;            // 1: rows via TMA gather4 into shared memory; 0: per-lane LDG gathers
   int ncb, box4;      // TMA: column blocks per row and float4s per block (DU = ncb * box4)
   int stage_bytes;    // shared memory per pipeline stage

@@ -42,6 +42,26 @@ __device__ __forceinline__ void st_out4(float* p, const float4& v) {
                : "memory");
 }
 
+// a5/a6 store of 4 pooled fp32 values at byte address p in the output element type: fp32 as one
+// 16-byte st.global.v4; bf16 / fp16 rounded to nearest even (R#32) and stored as 8 bytes.
+__device__ __forceinline__ void st_out_e4(char* p, float a, float b, float c, float d, int odt) {
+  if (odt == 0) {
+    st_out4(reinterpret_cast<float*>(p), make_float4(a, b, c, d));
+    return;
+  }
+  unsigned lo, hi;
+  if (odt == 1) {
+    const __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c, d);
+    lo = *reinterpret_cast<const unsigned*>(&x);
+    hi = *reinterpret_cast<const unsigned*>(&y);
+  } else {
+    const __half2 x = __floats2half2_rn(a, b), y = __floats2half2_rn(c, d);
+    lo = *reinterpret_cast<const unsigned*>(&x);
+    hi = *reinterpret_cast<const unsigned*>(&y);
+  }
+  asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p), "r"(lo), "r"(hi) : "memory");
+}
+
 __device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -287,7 +307,8 @@ __device__ __forceinline__ void pool_run_lsu(const uint4* __restrict__ tab, int 
                                              unsigned idx_s, const int* __restrict__ idx_g,
                                              unsigned w_s, const float* __restrict__ w_g,
                                              const int* so, int base, int b0, int b1, int lane,
-                                             bool mean, float* dst0, long long stride) {
+                                             bool mean, char* dst0, long long stride, int oshift,
+                                             int odt) {
   constexpr int EPU = Elem<ELEM>::EPU;
   float acc[NV][EPU];
 #pragma unroll
@@ -310,15 +331,15 @@ __device__ __forceinline__ void pool_run_lsu(const uint4* __restrict__ tab, int 
 #pragma unroll
         for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
     }
-    float* dst = dst0 + (long long)cb * stride;
+    char* dst = dst0 + (long long)cb * stride;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {                             // a6: zero-copy store
       const int c = lane + v * LPB;
       if (c < DU) {
 #pragma unroll
         for (int e = 0; e < EPU; e += 4)
-          st_out4(dst + EPU * c + e,
-                  make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+          st_out_e4(dst + ((long long)(EPU * c + e) << oshift), acc[v][e], acc[v][e + 1],
+                    acc[v][e + 2], acc[v][e + 3], odt);
       }
 #pragma unroll
       for (int e = 0; e < EPU; ++e) acc[v][e] = 0.f;
@@ -417,7 +438,7 @@ struct StageHdr {
   int remote;         // fused, s != r: count the stage's bags toward its slice when consumed
   int slice_id, slice_bags;
   long long j0;       // global sample of the first bag
-  float* out_base;    // fused: recv_s[parity]; pool: send
+  char* out_base;     // fused: recv_s[parity]; pool: send (elements of the output type)
   unsigned long long* flag;
 };
 
@@ -469,7 +490,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
   __shared__ int last_cta;
   // per-table and per-destination pointers, read once per CTA (no global round trip per stage)
   __shared__ const uint4* s_tab[kMaxSmemTables];
-  __shared__ float* s_out[kMaxW];
+  __shared__ char* s_out[kMaxW];
   __shared__ unsigned long long* s_flag[kMaxW];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane32 = tid & 31;
@@ -502,10 +523,10 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
     s_tab[i] = reinterpret_cast<const uint4*>(P.tables[i]);
   for (int i = tid; i < P.W; i += blockDim.x) {
     if (FUSED) {
-      s_out[i] = P.peers->recv[i][P.parity];
+      s_out[i] = reinterpret_cast<char*>(P.peers->recv[i][P.parity]);
       s_flag[i] = P.peers->flag_out[i];
     } else {
-      s_out[i] = P.send;
+      s_out[i] = reinterpret_cast<char*>(P.send);
       s_flag[i] = nullptr;
     }
   }
@@ -718,14 +739,16 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
                                             : reinterpret_cast<const uint4*>(P.tables[t]);
       // a5: bag b of this stage goes to row (row0 + b) of s's [b_s][G*D], column block
       // g = toff + t (fused), or to staging row (j0 + b), table t (pool)
-      float* dst0;
+      // (byte addresses: the output element is 4 or 2 bytes, P.oshift)
+      const int osh = P.oshift, odt = P.out_dtype;
+      char* dst0;
       long long stride;
       if (FUSED) {
-        dst0 = h->out_base + ((long long)h->row0 * P.G + (P.toff + t)) * D;
-        stride = (long long)P.G * D;
+        dst0 = h->out_base + ((((long long)h->row0 * P.G + (P.toff + t)) * D) << osh);
+        stride = ((long long)P.G * D) << osh;
       } else {
-        dst0 = h->out_base + (h->j0 * P.T + t) * (long long)D;
-        stride = (long long)P.T * D;
+        dst0 = h->out_base + (((h->j0 * P.T + t) * (long long)D) << osh);
+        stride = ((long long)P.T * D) << osh;
       }
       if (TMA && staged) {
         for (int b = group; b < nb; b += ngroups) {
@@ -741,15 +764,15 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
 #pragma unroll
               for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
           }
-          float* dst = dst0 + (long long)b * stride;
+          char* dst = dst0 + (long long)b * stride;
 #pragma unroll
           for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
             const int c = lane + v * LPB;
             if (c < P.DU) {
 #pragma unroll
               for (int e = 0; e < EPU; e += 4)
-                st_out4(dst + EPU * c + e,
-                        make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+                st_out_e4(dst + ((long long)(EPU * c + e) << osh), acc[v][e], acc[v][e + 1],
+                          acc[v][e + 2], acc[v][e + 3], odt);
             }
           }
         }
@@ -763,11 +786,11 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
           if (staged)
             pool_run_lsu<ELEM, LPB, NV, UF, true, WEIGHTED>(tab, P.DU, pay, nullptr, wpay, nullptr,
                                                             so, base, b0, b1, lane, P.mean != 0,
-                                                            dst0, stride);
+                                                            dst0, stride, osh, odt);
           else
             pool_run_lsu<ELEM, LPB, NV, UF, false, WEIGHTED>(
                 tab, P.DU, 0u, P.indices + base, 0u, WEIGHTED ? P.weights + base : nullptr, so,
-                base, b0, b1, lane, P.mean != 0, dst0, stride);
+                base, b0, b1, lane, P.mean != 0, dst0, stride, osh, odt);
         }
       } else {
         // long bags: one bag per lane group at a time, round robin, U rows in flight
@@ -788,15 +811,15 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
 #pragma unroll
               for (int e = 0; e < EPU; ++e) acc[v][e] = __fdiv_rn(acc[v][e], L);
           }
-          float* dst = dst0 + (long long)b * stride;
+          char* dst = dst0 + (long long)b * stride;
 #pragma unroll
           for (int v = 0; v < NV; ++v) {                         // a6: zero-copy store
             const int c = lane + v * LPB;
             if (c < P.DU) {
 #pragma unroll
               for (int e = 0; e < EPU; e += 4)
-                st_out4(dst + EPU * c + e,
-                        make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]));
+                st_out_e4(dst + ((long long)(EPU * c + e) << osh), acc[v][e], acc[v][e + 1],
+                          acc[v][e + 2], acc[v][e + 3], odt);
             }
           }
         }

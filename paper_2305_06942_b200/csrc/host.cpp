@@ -28,7 +28,7 @@ struct Meta {           // phase-1 all-gather record (problem statement, S:86-91
   int32_t rank, world, T, D;
   int64_t B;
   int64_t part[kMaxW + 1];
-  int32_t S, dtype, pooling, pad;
+  int32_t S, dtype, pooling, out_dtype;
 };
 
 struct Handles {        // phase-2 all-gather record (symmetric region)
@@ -103,6 +103,7 @@ struct emb_a2a {
   DevPeers* d_peers = nullptr;
   const void** d_tables = nullptr;
   int elem = 0;                          // table element type (emb_a2a_dtype)
+  int64_t out_dtype = 0;                 // output element type (option "out_dtype", R#32)
   int mean = 0;                          // pooling (emb_a2a_pooling)
   TmaDesc* d_tmaps = nullptr;            // one TMA descriptor per local table
   int ncb = 1, box4 = 1;
@@ -319,6 +320,8 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   P.weights = weights;
   P.elem = h->elem;
   P.mean = h->mean;
+  P.out_dtype = (int)h->out_dtype;
+  P.oshift = h->out_dtype == EMB_A2A_F32 ? 2 : 1;
   P.tables = h->d_tables;
   P.tmaps = h->d_tmaps;
   P.tma = (h->tma && h->elem == 0 && !weights) ? 1 : 0;   // TMA gather: fp32, unweighted
@@ -542,6 +545,7 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   me.S = (int32_t)h->S;
   me.dtype = table_dtype;
   me.pooling = pooling;
+  me.out_dtype = (int32_t)h->out_dtype;
   if (batch_partition) {
     for (int s = 0; s <= h->W; ++s) me.part[s] = batch_partition[s];
   } else if (h->W > 0 && global_batch % h->W == 0) {
@@ -563,10 +567,10 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
     if (m.magic != kMagic || m.abi != EMB_A2A_ABI_VERSION || m.rank != q || m.world != h->W)
       return fail(h, EMB_A2A_EINVAL, "rank %d sent invalid registration arguments", q);
     if (m.D != dim || m.B != global_batch || m.S != (int32_t)h->S || m.dtype != table_dtype ||
-        m.pooling != pooling ||
+        m.pooling != pooling || m.out_dtype != (int32_t)h->out_dtype ||
         memcmp(m.part, me.part, sizeof(int64_t) * (h->W + 1)) != 0)
       return fail(h, EMB_A2A_EINVAL,
-                  "ranks disagree on dim / global batch / partition / slice (rank %d)", q);
+                  "ranks disagree on dim / global batch / partition / slice / dtypes (rank %d)", q);
     G += m.T;
   }
   if (G < 1) return fail(h, EMB_A2A_EINVAL, "no tables registered on any rank");
@@ -596,7 +600,8 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
   //      (backward, fp32 tables only): [B][T_r][D] float32 gradient rows pushed by their
   //      data-parallel owners.  Credits: slot q counts the forwards (backwards) rank q started.
   const size_t flag_bytes = ((size_t)(4 * h->W + 1) * kFlagStride * 8 + 255) / 256 * 256;
-  const size_t buf_bytes = ((size_t)h->b * G * dim * 4 + 255) / 256 * 256;
+  const size_t oes = h->out_dtype == EMB_A2A_F32 ? 4 : 2;   // output element size (R#32)
+  const size_t buf_bytes = ((size_t)h->b * G * dim * oes + 255) / 256 * 256;
   auto gstage_bytes = [&](int Tq) -> size_t {
     if (table_dtype != EMB_A2A_F32) return 256;
     return std::max<size_t>(((size_t)Tq * global_batch * dim * 4 + 255) / 256 * 256, 256);
@@ -662,7 +667,7 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
     }
     const int64_t bq = h->part[q + 1] - h->part[q];
     const size_t fq = flag_bytes;   // identical layout on every rank (same W)
-    const size_t bufq = std::max<size_t>(((size_t)bq * G * dim * 4 + 255) / 256 * 256, 256);
+    const size_t bufq = std::max<size_t>(((size_t)bq * G * dim * oes + 255) / 256 * 256, 256);
     h->host_peers.recv[q][0] = (float*)(base + fq);
     h->host_peers.recv[q][1] = (float*)(base + fq + bufq);
     h->host_peers.flag_out[q] = (unsigned long long*)(base) + (size_t)h->rank * kFlagStride;
@@ -857,7 +862,7 @@ int emb_a2a_forward_host(emb_a2a_t* h, const int32_t* h_indices, const int32_t* 
                        nullptr, nullptr);
   if (rc) return rc;
   CUDA_TRY(h, cudaEventRecord(h->ev_free[par], st));
-  const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
+  const size_t out_bytes = (size_t)h->b * h->G * h->D * (h->out_dtype == EMB_A2A_F32 ? 4 : 2);
   if (out_bytes) CUDA_TRY(h, cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
   return EMB_A2A_OK;
 }
@@ -885,7 +890,7 @@ int emb_a2a_forward_host_batch(emb_a2a_t* h, int nsteps, const int32_t* const* h
   rc = host_staging(h, nmax);
   if (rc) return rc;
   const size_t noff = (size_t)h->T * h->B + 1;
-  const size_t out_bytes = (size_t)h->b * h->G * h->D * sizeof(float);
+  const size_t out_bytes = (size_t)h->b * h->G * h->D * (h->out_dtype == EMB_A2A_F32 ? 4 : 2);
   for (int k = 0; k < nsteps; ++k) {
     const int par = (int)(h->host_calls++ & 1);
     // inputs: copy stream, into the staging the forward two steps ago has finished reading
@@ -1275,7 +1280,8 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
   for (int q = 0; q < h->W; ++q) {
     if (q == h->rank) continue;
     const int64_t bq = h->part[q + 1] - h->part[q];
-    const int64_t half = std::max<int64_t>((bq * h->G * h->D * 4 + 255) / 256 * 256, 256);
+    const int64_t oes = h->out_dtype == EMB_A2A_F32 ? 4 : 2;
+    const int64_t half = std::max<int64_t>((bq * h->G * h->D * oes + 255) / 256 * 256, 256);
     cap = cap < 0 ? 2 * half : std::min<int64_t>(cap, 2 * half);
   }
   const long long runs = std::min<int64_t>(bytes_per_peer, cap) / 512;
@@ -1307,6 +1313,12 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (h->registered && v != h->order)   // slice ids (and their counters) depend on the order
       return fail(h, EMB_A2A_ESTATE, "set 'order' before register_tables");
     h->order = v;
+  } else if (k == "out_dtype") {
+    if (v < EMB_A2A_F32 || v > EMB_A2A_F16)
+      return fail(h, EMB_A2A_EINVAL, "out_dtype: 0 fp32, 1 bf16, 2 fp16");
+    if (h->registered && v != h->out_dtype)   // the receive buffers are sized for it
+      return fail(h, EMB_A2A_ESTATE, "set 'out_dtype' before register_tables");
+    h->out_dtype = v;
   } else if (k == "chunk") {
     if (v < 1 || v > 63) return fail(h, EMB_A2A_EINVAL, "chunk in [1, 63]");
     if (h->registered && v != h->chunk)
@@ -1393,6 +1405,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "idx_cap") *v = h->idx_cap;
   else if (k == "stages") *v = h->stages;
   else if (k == "chunk") *v = h->chunk;
+  else if (k == "out_dtype") *v = h->out_dtype;
   else if (k == "trace") *v = h->trace_cap;
   else if (k == "tma") *v = h->tma;
   else if (k == "vec") *v = h->vec;

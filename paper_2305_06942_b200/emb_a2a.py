@@ -73,11 +73,14 @@ class _CudaView:
                                          "data": (int(ptr), False), "version": 2, "strides": None}
 
 
-def _view(ptr: int, shape, device: torch.device) -> torch.Tensor:
+def _view(ptr: int, shape, device: torch.device, dtype=torch.float32) -> torch.Tensor:
     n = int(np.prod(shape)) if len(shape) else 1
     if n == 0 or ptr == 0:
-        return torch.empty(tuple(shape), dtype=torch.float32, device=device)
-    return torch.as_tensor(_CudaView(ptr, shape), device=device)
+        return torch.empty(tuple(shape), dtype=dtype, device=device)
+    if dtype == torch.float32:
+        return torch.as_tensor(_CudaView(ptr, shape), device=device)
+    # 16-bit outputs: __cuda_array_interface__ has no bfloat16 typestr; view the bits
+    return torch.as_tensor(_CudaView(ptr, shape, "<i2"), device=device).view(dtype)
 
 
 def _stream_ptr(stream, device) -> int:
@@ -168,6 +171,8 @@ class EmbA2A:
         self.D = D
         self.G = self.query("total_tables")
         self.b = self.query("local_batch")
+        self.out_dtype = {_lib.F32: torch.float32, _lib.BF16: torch.bfloat16,
+                          _lib.F16: torch.float16}[self.get_option("out_dtype")]
 
     _dim_hint = 4
 
@@ -178,7 +183,7 @@ class EmbA2A:
     def forward(self, indices: torch.Tensor, offsets: torch.Tensor, stream=None,
                 per_sample_weights: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Fused forward; returns a zero-copy view [b_r, G*D] of the library-owned receive buffer
-        (valid until the second following forward).  per_sample_weights: optional float32 device
+        (valid until the second following forward), float32 or the "out_dtype" option's type.  per_sample_weights: optional float32 device
         tensor aligned with indices (sum pooling only)."""
         if offsets.dtype != torch.int32 or indices.dtype != torch.int32 or \
                 offsets.device != self.device or indices.device != self.device or \
@@ -203,7 +208,7 @@ class EmbA2A:
         key = (out.value or 0, rows.value, cols.value)
         v = self._views.get(key)
         if v is None:
-            v = self._views[key] = _view(key[0], key[1:], self.device)
+            v = self._views[key] = _view(key[0], key[1:], self.device, self.out_dtype)
         return v
 
     def forward_host(self, indices: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor,
@@ -211,7 +216,7 @@ class EmbA2A:
         """End-to-end forward from host (pinned) int32 tensors into host float32 out [b_r, G*D];
         asynchronous on `stream` -- synchronise before reading `out`."""
         for t, dt, n in ((indices, torch.int32, "indices"), (offsets, torch.int32, "offsets"),
-                         (out, torch.float32, "out")):
+                         (out, self.out_dtype, "out")):
             if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous():
                 raise ValueError(f"{n} must be a contiguous host {dt} tensor")
         rc = lib.emb_a2a_forward_host(self._h, indices.data_ptr() if indices.numel() else None,
@@ -269,7 +274,7 @@ class EmbA2A:
             raise ValueError("indices, offsets and outs must have one entry per step")
         for k in range(n):
             for t, dt, nm in ((indices[k], torch.int32, "indices"), (offsets[k], torch.int32, "offsets"),
-                              (outs[k], torch.float32, "outs")):
+                              (outs[k], self.out_dtype, "outs")):
                 if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous():
                     raise ValueError(f"{nm}[{k}] must be a contiguous host {dt} tensor")
         P = ctypes.c_void_p * max(n, 1)
@@ -306,8 +311,9 @@ class EmbA2A:
     # -------------------------------------------------------------- local API
     def pool_local(self, indices: torch.Tensor, offsets: torch.Tensor, send: torch.Tensor,
                    stream=None, per_sample_weights: Optional[torch.Tensor] = None) -> None:
-        """Unfused baseline first half: send [B, T_r, D] float32 (dest-major blocks by p_s)."""
-        _check_dev_tensor(send, torch.float32, "send", self.device)
+        """Unfused baseline first half: send [B, T_r, D] of the output type (dest-major blocks by
+        p_s)."""
+        _check_dev_tensor(send, self.out_dtype, "send", self.device)
         _check_dev_tensor(offsets, torch.int32, "offsets", self.device)
         _check_dev_tensor(indices, torch.int32, "indices", self.device)
         n = indices.numel()
