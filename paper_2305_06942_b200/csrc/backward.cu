@@ -126,8 +126,9 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
           S.keys[p] = key;
           S.bags[p] = (int)bag;
           if (WEIGHTED) S.wts[p] = wv[u];
-          for (int q = 0; q < S.passes; ++q)
-            atomicAdd(&h[q * 256 + ((key >> (8 * q)) & 255u)], 1u);
+          for (int q = 0; q < S.passes; ++q)   // row bits only: the last digit may be narrower
+            atomicAdd(&h[q * 256 + ((key >> (8 * q)) & (q == S.passes - 1 ? S.last_mask : 255u))],
+                      1u);
         }
       }
     }
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
-    const unsigned d = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
+    const unsigned d = pos < P.n ? ((key[i] >> P.shift) & P.dmask) : 256u;
     peers[i] = __match_any_sync(kFull, d);
     if (d < 256u && lane == __ffs(peers[i]) - 1) atomicAdd(&s_hist[d], __popc(peers[i]));
   }
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
-    const unsigned dd = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
+    const unsigned dd = pos < P.n ? ((key[i] >> P.shift) & P.dmask) : 256u;
     const unsigned c = dd < 256u ? s_cnt[w][dd] : 0u;
     rank[i] = (unsigned short)(c + __popc(peers[i] & lt_mask));
     __syncwarp();
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
     if (pos < P.n) {
-      const unsigned dd = (key[i] >> P.shift) & 255u;
+      const unsigned dd = (key[i] >> P.shift) & P.dmask;
       const unsigned lp = s_tstart[dd] + s_cnt[w][dd] + rank[i];
       s_key[lp] = key[i];
       s_bag[lp] = bag[i];
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_kernel(const PassPa
   const int tn = (P.n - t0) < kSortTile ? (int)(P.n - t0) : kSortTile;
   for (int i = tid; i < tn; i += kSortThreads) {
     const unsigned k = s_key[i];
-    const unsigned dd = (k >> P.shift) & 255u;
+    const unsigned dd = (k >> P.shift) & P.dmask;
     const unsigned out = s_gofs[dd] + (unsigned)i - s_tstart[dd];
     P.keys_out[out] = k;
     P.bags_out[out] = s_bag[i];
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_upsweep_kernel(const PassPar
   const long long t0 = (long long)blockIdx.x * kSortTile;
   for (int i = tid; i < kSortTile; i += kSortThreads) {
     const long long pos = t0 + i;
-    if (pos < P.n) atomicAdd(&h[(P.keys_in[pos] >> P.shift) & 255u], 1u);
+    if (pos < P.n) atomicAdd(&h[(P.keys_in[pos] >> P.shift) & P.dmask], 1u);
   }
   __syncthreads();
   P.cnt[(long long)tid * P.ntiles + blockIdx.x] = h[tid];
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassP
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
-    const unsigned dg = pos < P.n ? ((key[i] >> P.shift) & 255u) : 256u;
+    const unsigned dg = pos < P.n ? ((key[i] >> P.shift) & P.dmask) : 256u;
     const unsigned peers = __match_any_sync(kFull, dg);
     const unsigned c = dg < 256u ? s_cnt[w][dg] : 0u;
     rank[i] = (unsigned short)(c + __popc(peers & lt_mask));
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassP
   for (int i = 0; i < kSortItems; ++i) {
     const long long pos = base + i * 32 + lane;
     if (pos < P.n) {
-      const unsigned dd = (key[i] >> P.shift) & 255u;
+      const unsigned dd = (key[i] >> P.shift) & P.dmask;
       const unsigned lp = s_tstart[dd] + s_cnt[w][dd] + rank[i];
       s_key[lp] = key[i];
       s_bag[lp] = bag[i];
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassP
   const int tn = (P.n - t0) < kSortTile ? (int)(P.n - t0) : kSortTile;
   for (int i = tid; i < tn; i += kSortThreads) {
     const unsigned k = s_key[i];
-    const unsigned dd = (k >> P.shift) & 255u;
+    const unsigned dd = (k >> P.shift) & P.dmask;
     const unsigned out = s_gofs[dd] + (unsigned)i - s_tstart[dd];
     P.keys_out[out] = k;
     P.bags_out[out] = s_bag[i];
@@ -537,11 +538,13 @@ template <int NVC, int MODE>
 __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_kernel(const __grid_constant__ BwdParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_pushed[kMaxW];
+  __shared__ unsigned long long s_ready;     // sources whose rows of this epoch have all landed
   __shared__ float* s_tab[kMaxSmemTables];   // this rank's table pointers (T <= 256)
   __shared__ long long s_ticket[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int D = P.D, DU = D >> 2;
 
+  if (tid == 0) s_ready = 0ull;
   pdl_wait();     // the plan (sort) and the caller's gradient are complete
   pdl_trigger();
   btrace(P, 20, 0);
@@ -607,26 +610,9 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
         red_release_sys_add(P.peers->bflag_out[q], (unsigned long long)s_pushed[q]);
       }
     }
-    // a8 (reverse): every source's rows of this epoch have landed here
-    if (tid == 0 && P.T > 0) {
-      for (int s = 0; s < P.W; ++s) {
-        if (s == P.r) continue;
-        const unsigned long long target =
-            P.bepoch * (unsigned long long)(P.part[s + 1] - P.part[s]);
-        const unsigned long long* f = P.bflags_in + (size_t)s * kFlagStride;
-        const unsigned long long t0 = globaltimer();
-        unsigned backoff = 32;
-        while (ld_acquire_sys(f) < target) {
-          if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
-            atomicExch(P.err, 0x400 | s);
-            break;
-          }
-          __nanosleep(backoff);
-          if (backoff < 1024) backoff <<= 1;
-        }
-      }
-    }
-    __syncthreads();
+    // a8 (reverse) is per source and per warp (below): a warp waits for source s's rows only
+    // when a lookup of its sub-batch needs them, so the reduction of rows from sources that have
+    // arrived (and of this rank's own rows) overlaps the exchange from the others.
   }
   if (P.T == 0 || P.n == 0) return;
   for (int t = tid; t < P.T && t < kMaxSmemTables; t += blockDim.x) s_tab[t] = P.tables[t];
@@ -702,12 +688,14 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
       const bool out_sb = last_sb ? chunk_out : (__shfl_sync(kFull, nkey, 0) == keyl);
       const int npieces = __popc(startm);
       __syncwarp();                                  // the previous sub-batch's readers are done
+      unsigned long long needm = 0ull;               // remote sources this sub-batch reads
       if (lane < len) {
         const unsigned t = P.rbits >= 32 ? 0u : key >> P.rbits;   // bag = t * B + j
         const long long j = (long long)((unsigned)bag - t * B32);
         int s = 0;
         if (P.W > 1)
           while (P.part[s + 1] <= j) ++s;            // destination of bag j
+        if (P.fused && s != P.r) needm = 1ull << s;
         const float* src;
         if (P.fused)
           src = (s == P.r) ? P.grad + ((j - pr) * P.G + P.toff + (int)t) * D
@@ -726,6 +714,39 @@ __global__ void __launch_bounds__(128, NVC >= 8 ? 1 : (NVC == 1 ? 6 : 4)) bwd_ke
                              reinterpret_cast<const char*>(trow) + b));
         if (MODE == 1) wsc[lane] = P.wts[pb + lane];
         if (MODE == 2) wsc[lane] = (float)(P.offsets[bag + 1] - P.offsets[bag]);
+      }
+      if (P.fused && P.W > 1) {
+        // a8 (reverse), per source: rows from source s are read only once all of s's rows of
+        // this epoch have landed (its counter reached bepoch * b_s, ld.acquire.sys); the first
+        // warp of the CTA to see it records it for the others
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) needm |= __shfl_xor_sync(kFull, needm, o);
+        const unsigned long long miss = needm & ~*(volatile unsigned long long*)&s_ready;
+        if (miss) {
+          if (lane == 0) {
+            for (unsigned long long m = miss; m; m &= m - 1) {
+              const int src = __ffsll((long long)m) - 1;
+              const unsigned long long target =
+                  P.bepoch * (unsigned long long)(P.part[src + 1] - P.part[src]);
+              const unsigned long long* f = P.bflags_in + (size_t)src * kFlagStride;
+              const unsigned long long t0 = globaltimer();
+              unsigned backoff = 32;
+              while (ld_acquire_sys(f) < target) {
+                if (globaltimer() - t0 > (unsigned long long)P.timeout_ns) {
+                  atomicExch(P.err, 0x400 | src);
+                  break;
+                }
+                __nanosleep(backoff);
+                if (backoff < 1024) backoff <<= 1;
+              }
+            }
+            fence_acq_rel_sys();
+            atomicOr(&s_ready, miss);
+          }
+        } else {
+          // another warp's acquire covers these sources: order our loads after it
+          asm volatile("fence.acq_rel.cta;" ::: "memory");
+        }
       }
       if (sb == 0 && lane == 0) {
         const bool inside = chunk_in && chunk_out && npieces == 1 && nsb == 1;

@@ -169,7 +169,9 @@ cudaError_t launch_validate(const int* indices, const int* offsets, long long nn
 
 // ------------------------------------------------------------------------------ backward (f3)
 // Sort plan: this rank's lookups as (key = t << rbits | row, payload = bag id t*B + j [, weight])
-// sorted stably by key with an LSD radix sort (8-bit digits, one onesweep pass per digit).
+// sorted stably by the ROW bits of the key with an LSD radix sort (8-bit digits, one onesweep
+// pass per digit).  The lookups arrive table-major, so the stable sort by row alone leaves each
+// (table, row) run contiguous and in ascending lookup order (R#31): the table bits need no pass.
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
@@ -188,6 +190,7 @@ struct SortParams {
   unsigned* hist_clear;        // the other half of the plan buffer: zeroed here for the next plan
   long long TB, B;
   int rbits, passes;
+  unsigned last_mask;          // digit mask of the last pass (row bits only: may be < 8 bits)
   unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)
   long long lbg_words;
 };
@@ -208,6 +211,7 @@ struct PassParams {
   long long ntiles;
   long long n;
   int shift;
+  unsigned dmask;              // this pass's digit mask (255, or narrower for the last pass)
   unsigned stamp;              // plan number (30 bits): stale look-back words are ignored
   unsigned long long* trace;   // optional %globaltimer event log (the "trace" option)
   long long trace_cap;

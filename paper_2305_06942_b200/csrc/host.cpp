@@ -1095,7 +1095,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     if (rc) return rc;
   }
   const int64_t n = (h->T > 0) ? num_indices : 0;
-  const int passes = (tbits + rbits + 7) / 8;
+  // passes over the row bits only (the input is table-major and the sort stable, R#31)
+  const int passes = (rbits + 7) / 8;
   const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
@@ -1169,6 +1170,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   S.B = h->B;
   S.rbits = rbits;
   S.passes = passes;
+  S.last_mask = passes > 0 ? (1u << (rbits - 8 * (passes - 1))) - 1u : 0u;
   S.lbg = h->d_lbg;
   S.lbg_words = (long long)nlbg;
   PassParams pp[kMaxPasses];
@@ -1190,6 +1192,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.ntiles = ntiles;
     q.n = n;
     q.shift = 8 * p;
+    q.dmask = p == passes - 1 ? S.last_mask : 255u;
     q.stamp = h->plan_no;
     q.trace = h->d_trace;
     q.trace_cap = h->trace_cap;
