@@ -13,25 +13,31 @@
 // Kernels:
 //   bwd_keygen_kernel    key_k = t << rbits | idx_k, payload bag_k (+ w_k); digit histograms of
 //                        every radix pass at once (upfront histogram)
+//   bwd_onesweep_kernel  one stable LSD radix pass (8-bit digit) in one kernel, with a two-level
+//                        look-back over the tiles (used while the tiles fit one wave)
 //   bwd_upsweep_kernel / bwd_scan_kernel / bwd_downsweep_kernel
-//                        one stable LSD radix pass (8-bit digit), reduce-then-scan: tile digit
-//                        counts, a per-digit scan over tiles, then warp-level ranking with
-//                        match.any and a digit-ordered, contiguous write-out of each tile
-//   bwd_kernel           (fused) each CTA first pushes its share of this rank's gradient rows
-//                        straight into the owners' staging buffers over NVLink (zero-copy, the
-//                        reverse of P:165) and signals the owner's per-source counter with
-//                        red.release.sys; then waits (ld.acquire.sys) for every source's rows;
-//                        then reduces: the sorted lookups are cut into chunks of C; a warp
-//                        gathers a chunk's gradient rows and the table rows it will update into
-//                        shared memory (cp.async), sums each run of equal keys in order (lane
-//                        groups take different runs when a row needs fewer than 32 lanes), and
-//                        updates the row.  A run that crosses chunks leaves one partial sum per
-//                        chunk it touches and counts it on the run's counter; whichever chunk
-//                        completes the count folds the partials in chunk order and updates the
-//                        row (the last-finisher pattern of P:149/P:176, with a fixed fold order,
-//                        so the result does not depend on who finishes last).  No warp waits.
+//                        the same pass as reduce-then-scan: tile digit counts, a per-digit scan
+//                        over tiles, then warp-level ranking with match.any and a digit-ordered,
+//                        contiguous write-out of each tile (more tiles than one wave)
+//   bwd_kernel           pass 1 (fused) each CTA first pushes its share of this rank's gradient
+//                        rows straight into the owners' staging buffers over NVLink (zero-copy,
+//                        the reverse of P:165; a store into owner q waits for q's credit) and
+//                        signals the owner's per-source counter with red.release.sys once per
+//                        (CTA, owner).  No CTA-wide wait: a warp reads source s's rows only after
+//                        s's counter shows all of them landed (ld.acquire.sys, per warp and
+//                        source, recorded in shared memory for the CTA's other warps), so the
+//                        reduction overlaps the exchange.  Reduce: the sorted lookups are cut
+//                        into chunks; a warp walks a chunk's runs 32 lookups at a time (lane
+//                        groups take different runs when a row needs fewer than 32 lanes), sums
+//                        each run in ascending lookup order and applies the SGD step to rows
+//                        whose run starts and ends inside the chunk; a run crossing chunk edges
+//                        leaves one partial sum per chunk in scratch.
 //                        (local) the same reduce from a caller-owned [B][T][D] gradient -- the
 //                        unfused baseline's second half after NCCL all_to_all_single.
+//   bwd_fold_kernel / bwd_fold_narrow_kernel
+//                        pass 2: the chunk a crossing run starts in folds the partials in chunk
+//                        order (fixed order: the result does not depend on timing) and updates
+//                        the row.  The kernel boundary orders pass 1's partials before it.
 #include "fused_kernel.cuh"
 
 namespace emba2a {
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
           S.keys[p] = key;
           S.bags[p] = (int)bag;
           if (WEIGHTED) S.wts[p] = wv[u];
-          for (int q = 0; q < S.passes; ++q)   // row bits only: the last digit may be narrower
+          for (int q = 0; q < S.passes; ++q)   // the last digit may be narrower
             atomicAdd(&h[q * 256 + ((key >> (8 * q)) & (q == S.passes - 1 ? S.last_mask : 255u))],
                       1u);
         }

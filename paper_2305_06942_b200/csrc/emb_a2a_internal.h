@@ -169,9 +169,8 @@ cudaError_t launch_validate(const int* indices, const int* offsets, long long nn
 
 // ------------------------------------------------------------------------------ backward (f3)
 // Sort plan: this rank's lookups as (key = t << rbits | row, payload = bag id t*B + j [, weight])
-// sorted stably by the ROW bits of the key with an LSD radix sort (8-bit digits, one onesweep
-// pass per digit).  The lookups arrive table-major, so the stable sort by row alone leaves each
-// (table, row) run contiguous and in ascending lookup order (R#31): the table bits need no pass.
+// sorted stably by key with an LSD radix sort (8-bit digits, one onesweep pass per digit; the
+// last digit may be narrower).
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
@@ -190,7 +189,7 @@ struct SortParams {
   unsigned* hist_clear;        // the other half of the plan buffer: zeroed here for the next plan
   long long TB, B;
   int rbits, passes;
-  unsigned last_mask;          // digit mask of the last pass (row bits only: may be < 8 bits)
+  unsigned last_mask;          // digit mask of the last pass (the key may end inside a digit)
   unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)
   long long lbg_words;
 };

@@ -1095,8 +1095,12 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     if (rc) return rc;
   }
   const int64_t n = (h->T > 0) ? num_indices : 0;
-  // passes over the row bits only (the input is table-major and the sort stable, R#31)
-  const int passes = (rbits + 7) / 8;
+  // passes over the whole key (table, row).  (Measured: sorting the row bits only -- the input
+  // is table-major and the sort stable, so (table, row) runs stay contiguous -- saves a pass for
+  // DLRM-wide / sweep / weak, but the (row, table) order it leaves makes the reduction jump
+  // between tables: pass 1 of DLRM-wide 401 -> 451 us, more than the plan saved.)
+  const int kbits = tbits + rbits;
+  const int passes = (kbits + 7) / 8;
   const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
@@ -1170,7 +1174,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   S.B = h->B;
   S.rbits = rbits;
   S.passes = passes;
-  S.last_mask = passes > 0 ? (1u << (rbits - 8 * (passes - 1))) - 1u : 0u;
+  S.last_mask = passes > 0 ? (1u << (kbits - 8 * (passes - 1))) - 1u : 0u;
   S.lbg = h->d_lbg;
   S.lbg_words = (long long)nlbg;
   PassParams pp[kMaxPasses];

@@ -33,8 +33,9 @@ def test_fixed_pooling_factor():
 
 
 def test_zipf_rank_frequency_slope():
-    """log-frequency vs log-rank slope of the top ranks ~ -alpha (before the row bijection the
-    rank is recoverable because A, C are fixed per table: count row frequencies instead)."""
+    """log-frequency vs log-rank slope of the top ranks ~ -alpha.  The rank -> row bijection
+    (A, C drawn per (batch, table) substream) only renames rows, so the sorted row frequencies of
+    one (batch, table) draw are the rank frequencies."""
     cfg = synth.config_for("dlrm_small", W=1, R=100_000, B=20000)
     L, rows = synth.dlrm_gen.gen_table_bags(cfg, 0, 0)
     cnt = np.sort(np.bincount(rows, minlength=cfg.R))[::-1].astype(np.float64)
