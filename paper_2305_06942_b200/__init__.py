@@ -7,8 +7,10 @@ counters with system-scope release/acquire, inside one sm_100a kernel.
 
 Public API: EmbA2A (one rank), LoopbackGroup (W virtual ranks on one device), LocalGroup /
 torch_allgather (bootstrap channels).  C ABI: include/emb_a2a.h, libemba2a.so.
+Row f4: AgGemm / AgGemmLoopback, the fused AllGather + GEMM (include/ag_gemm.h).
 """
 from ._lib import LIB_PATH, EXPORTED  # noqa: F401  (raises if the library is not built)
 from .emb_a2a import (EmbA2A, EmbA2AError, LocalGroup, run_ranks,  # noqa: F401
                       torch_allgather)
 from .loopback import LoopbackGroup  # noqa: F401
+from .ag_gemm import AgGemm, AgGemmLoopback  # noqa: F401  (SURVEY.md Sec 8 f4, P:180)

@@ -61,7 +61,23 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
-for _name, (_res, _args) in _SIGS.items():
+# include/ag_gemm.h: the fused AllGather + GEMM
+_AG_SIGS = {
+    "ag_gemm_init": (_I, [_I, _I, _I, ALLGATHER_FN, _P, ctypes.POINTER(_P)]),
+    "ag_gemm_register": (_I, [_P, _I64, _I64, _I64, _I]),
+    "ag_gemm_forward": (_I, [_P, _P, _P, _P, _P, ctypes.POINTER(_P)]),
+    "ag_gemm_set_option": (_I, [_P, ctypes.c_char_p, _I64]),
+    "ag_gemm_get_option": (_I, [_P, ctypes.c_char_p, _PI64]),
+    "ag_gemm_query": (_I, [_P, ctypes.c_char_p, _PI64]),
+    "ag_gemm_read_flags": (_I, [_P, _P, _I64, _PI64]),
+    "ag_gemm_check": (_I, [_P]),
+    "ag_gemm_destroy": (_I, [_P]),
+    "ag_gemm_last_error": (ctypes.c_char_p, [_P]),
+}
+AG_EXPORTED = tuple(_AG_SIGS)
+_SIGS_ALL = dict(_SIGS, **_AG_SIGS)
+
+for _name, (_res, _args) in _SIGS_ALL.items():
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args

@@ -23,6 +23,11 @@ def _load():
         _lib.synth_fill_table.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int,
                                           ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_int,
                                           ctypes.c_void_p]
+        _lib.synth_fill_gemm_bf16.restype = ctypes.c_int
+        _lib.synth_fill_gemm_bf16.argtypes = [ctypes.c_void_p, ctypes.c_longlong,
+                                              ctypes.c_longlong, ctypes.c_longlong,
+                                              ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_int,
+                                              ctypes.c_void_p]
     return _lib
 
 
@@ -42,3 +47,12 @@ def rank_tables(cfg: ProblemConfig, r: int, device) -> List[torch.Tensor]:
     for t, tab in enumerate(tabs):
         fill_table(tab, cfg.toff(r) + t, cfg.table_seed, cfg.value_mode)
     return tabs
+
+
+def fill_gemm_bf16(dst: torch.Tensor, tensor: int, seed: int, mode: int, row0: int = 0) -> None:
+    """Fill a [rows][cols] bf16 tensor with the GEMM operand generator (synth/gemm_gen.py)."""
+    assert dst.is_cuda and dst.dtype == torch.bfloat16 and dst.is_contiguous() and dst.dim() == 2
+    rc = _load().synth_fill_gemm_bf16(dst.data_ptr(), dst.shape[0], dst.shape[1], row0, tensor,
+                                      seed, mode, torch.cuda.current_stream(dst.device).cuda_stream)
+    if rc:
+        raise RuntimeError(f"synth_fill_gemm_bf16 failed ({rc})")

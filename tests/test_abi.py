@@ -57,3 +57,17 @@ def test_sm100a_sass_in_library():
         return
     out = subprocess.run([exe, "--list-elf", p.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_ag_gemm_library_exports_every_declared_symbol():
+    """include/ag_gemm.h: every declared entry point is exported and bound."""
+    import paper_2305_06942_b200 as p
+    from paper_2305_06942_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "ag_gemm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(ag_gemm_\w+)\s*\(", src, flags=re.M))
+    names.discard("ag_gemm_allgather_fn")
+    assert {"ag_gemm_init", "ag_gemm_register", "ag_gemm_forward", "ag_gemm_destroy"} <= names
+    lib = ctypes.CDLL(p.LIB_PATH)
+    assert not [n for n in names if not hasattr(lib, n)]
+    assert names == set(_lib.AG_EXPORTED)
