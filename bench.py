@@ -66,6 +66,12 @@ def parse():
                     help="skip the alpha = 0 (uniform, cold-cache) control leg")
     ap.add_argument("--alpha0-batches", type=int, default=4)
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    ap.add_argument("--path", default="emb_a2a", choices=["emb_a2a", "ag_gemm"],
+                    help="emb_a2a: the north-star fused embedding + All-to-All (default); "
+                         "ag_gemm: SURVEY Sec 8 row f4, the fused AllGather + GEMM (P:180)")
+    ap.add_argument("--ag-config", default="ag_ffn", help="ag_gemm workload (synth/gemm_gen.py)")
+    ap.add_argument("--ag-order", type=int, default=-1, help="ag_gemm tile order (0 comm-aware, 1 ascending)")
+    ap.add_argument("--ag-grid", type=int, default=0, help="ag_gemm persistent CTAs (0 = auto)")
     return ap.parse_args()
 
 
@@ -300,6 +306,10 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.path == "ag_gemm":
+        import bench_ag_gemm
+        return bench_ag_gemm.main(args, ROOT, {"ClockSampler": ClockSampler, "host_cpu": host_cpu,
+                                               "dist_env": dist_env})
     if args.impl == "reference":
         return run_reference(args)
 
