@@ -93,3 +93,46 @@ def gpu_ipc_worker(rank, world, port, q):
     h.destroy()
     q.put((rank, ok and ok_bwd, ok_flags))
     dist.destroy_process_group()
+
+
+def gpu_ag_ipc_worker(rank, world, port, q):
+    """Fused AllGather + GEMM across processes on ONE GPU: each process maps
+    the other's gather buffer with cudaIpcOpenMemHandle; exact-int operands, three forwards
+    (both buffer halves, credits across the process boundary), bitwise against the oracle."""
+    import numpy as np
+    import torch
+    dist = init_gloo(rank, world, port)
+    from oracle import ag_gemm as O
+    from synth import gemm_gen as G
+    from synth.device import fill_gemm_bf16
+    from paper_2305_06942_b200 import AgGemm, torch_allgather
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    cfg = G.GemmConfig("mp", world, 256, 256, 512, 1)
+    X = torch.empty((cfg.M, cfg.K), dtype=torch.bfloat16, device=dev)
+    Wr = torch.empty((cfg.N_r, cfg.K), dtype=torch.bfloat16, device=dev)
+    fill_gemm_bf16(X, G.X_TENSOR + rank, G.GEMM_SEED, 1)
+    fill_gemm_bf16(Wr, G.W_TENSOR + rank, G.GEMM_SEED, 1)
+    h = AgGemm(rank, world, dev, torch_allgather(), {"timeout_ms": 60000})
+    h.register(cfg.M, cfg.N_r, cfg.K)
+    shared = h.query("shared_gpu") == 1
+    ok = True
+    Xh, _ = G.rank_inputs(cfg, rank)
+    Wf, Yref = O.ag_gemm(Xh, [G.rank_inputs(cfg, s)[1] for s in range(world)])
+    for _ in range(3):
+        Y, Wg = h.forward(X, Wr)
+        torch.cuda.synchronize()
+        h.check()
+        ok &= bool(np.array_equal(Y.view(torch.int16).cpu().numpy().view(np.uint16),
+                                  O.bf16_rne_bits(Yref)))
+        wg = Wg.view(torch.int16).cpu().numpy().view(np.uint16)
+        for s in range(world):
+            if s != rank:
+                blk = slice(s * cfg.N_r, (s + 1) * cfg.N_r)
+                ok &= bool(np.array_equal(wg[blk], G.to_bf16_bits_exact(Wf[blk])))
+        dist.barrier()
+    flags = h.read_flags()
+    ok_flags = bool(all((flags[s] == 3).all() for s in range(world) if s != rank))
+    h.destroy()
+    q.put((rank, ok and shared, ok_flags))
+    dist.destroy_process_group()

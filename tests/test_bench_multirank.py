@@ -66,3 +66,25 @@ def test_ablations_command_torchrun_shared_gpu():
         assert rec["us_per_step"] > 0 and rec["parity"]["within_tol"] is True
     kinds = [next(iter(rec["ablation"])) for rec in recs]
     assert kinds == ["E4", "E4", "E3"] + ["E5"] * 6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2])
+def test_bench_ag_gemm_torchrun_shared_gpu(n):
+    """bench.py --path ag_gemm under torchrun (f4): per-rank oracle parity, the NCCL-style
+    baseline leg, e2e and the tensor roofline keys, max over ranks."""
+    env = dict(os.environ, EMBA2A_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--path", "ag_gemm", "--ag-config", "ag_tiny",
+           "--gpus", str(n), "--steps", "4", "--warmup", "3", "--cpu-seconds", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == n and line["value"] > 0 and line["unit"] == "TFLOP/s"
+    assert line["parity_all_ranks"] is True and line["parity"]["gathered_bitwise"] is True
+    assert line["roofline"]["bound"] == "tensor" and line["roofline"]["frac"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["cpu_baseline"]["value"] > 0
+    assert line["unfused"]["ms_per_step"] > 0

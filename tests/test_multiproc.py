@@ -43,3 +43,11 @@ def test_two_processes_one_gpu_cuda_ipc_path():
     tables exactly as the oracle does."""
     for rank, ok, ok_flags in run(_mp_worker.gpu_ipc_worker, 2, timeout=300):
         assert ok and ok_flags, rank
+
+
+@pytest.mark.gpu
+def test_two_processes_one_gpu_ag_gemm_cuda_ipc():
+    """f4 across processes: chunk PUTs into the other process's gather buffer, ready flags and
+    credits through cudaIpc mappings; three forwards bitwise equal to the oracle."""
+    for rank, ok, ok_flags in run(_mp_worker.gpu_ag_ipc_worker, 2, timeout=300):
+        assert ok and ok_flags, rank
