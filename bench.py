@@ -72,6 +72,9 @@ def parse():
     ap.add_argument("--ag-config", default="ag_ffn", help="ag_gemm workload (synth/gemm_gen.py)")
     ap.add_argument("--ag-order", type=int, default=-1, help="ag_gemm tile order (0 comm-aware, 1 ascending)")
     ap.add_argument("--ag-grid", type=int, default=0, help="ag_gemm persistent CTAs (0 = auto)")
+    ap.add_argument("--ag-leg", type=int, default=-1,
+                    help="add the f4 AllGather+GEMM measurement to the main line as 'ag_gemm' "
+                         "(-1 = only at N=1, 0 = never, 1 = at every N)")
     return ap.parse_args()
 
 
@@ -621,6 +624,22 @@ def main():
                            lambda v: all_gather_floats(v, dist, shared, dev),
                            weights=None if w_all0 is None else [w_all0], pooling=args.pooling)
 
+    ag = None
+    if (args.ag_leg == 1 or (args.ag_leg == -1 and N == 1)) and args.timing == "b2b":
+        # the fused AllGather + GEMM, its own metric (TFLOP/s); the full
+        # line is `bench.py --path ag_gemm`.  Measured after the main path, outside its timing.
+        try:
+            import bench_ag_gemm
+            agl = bench_ag_gemm.measure(args, ROOT, dev, rank, N, shared, ClockSampler, host_cpu,
+                                        "ag_tiny" if shared else args.ag_config,
+                                        min(args.steps, 10), 3, with_e2e=False, with_cpu=False)
+            ag = {"metric": agl["metric"], "value": agl["value"], "unit": agl["unit"],
+                  "ms_per_step": agl["ms_per_step"], "workload": agl["config"]["workload"],
+                  "roofline": agl["roofline"], "unfused": agl["unfused"],
+                  "parity_all_ranks": agl["parity_all_ranks"], "clocks": agl["clocks"],
+                  "gpu_launches": agl["gpu_launches"], "full_line": "bench.py --path ag_gemm"}
+        except Exception as e:     # reported, never fatal for the main path's line
+            ag = {"error": repr(e)[:400]}
     line = {
         "metric": METRIC,
         "value": value, "unit": "lookups/s", "n_gpus": N, "steps": args.steps,
@@ -655,6 +674,7 @@ def main():
         "parity": parity, "alpha0": alpha0, "nvlink_probe": nvl,
         "flushed": flushed, "clocks": clocks, "gpu_launches": int(launches),
         "backward": backward,
+        "ag_gemm": ag,
     }
     if shared:
         line["test_mode"] = "EMBA2A_SHARED_GPU=1: all ranks on one GPU; not a bench value"

@@ -82,7 +82,10 @@ def run_reference(args, root, host_cpu):
     print(json.dumps(line), flush=True)
 
 
-def main(args, root, helpers):
+def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, steps, warmup,
+            with_e2e=True, with_cpu=True):
+    """One AllGather + GEMM measurement on an initialised process group; returns the JSON dict
+    (rank 0's view; timings are max over ranks, parity is min over ranks)."""
     import torch
     import torch.distributed as dist
 
@@ -91,32 +94,8 @@ def main(args, root, helpers):
     from synth import gemm_gen as G
     from synth.device import fill_gemm_bf16
 
-    ClockSampler, host_cpu, dist_env = helpers["ClockSampler"], helpers["host_cpu"], helpers["dist_env"]
-    if args.impl == "reference":
-        return run_reference(args, root, host_cpu)
-    rank, world, local = dist_env()
-    N = world
-    if args.gpus != world and world == 1 and args.gpus > 1:
-        raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
-    shared = os.environ.get("EMBA2A_SHARED_GPU") == "1"
-    if shared:
-        local = 0
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if "MASTER_PORT" not in os.environ:
-            import socket
-            s = socket.socket()
-            s.bind(("127.0.0.1", 0))
-            os.environ["MASTER_PORT"] = str(s.getsockname()[1])
-            s.close()
-        if shared:
-            dist.init_process_group("gloo", rank=rank, world_size=world)
-        else:
-            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-
-    cfg = G.gemm_config(args.ag_config, N, mode=0)
+    local = dev.index or 0
+    cfg = G.gemm_config(cfg_name, N, mode=0)
     X = torch.empty((cfg.M, cfg.K), dtype=torch.bfloat16, device=dev)
     Wr = torch.empty((cfg.N_r, cfg.K), dtype=torch.bfloat16, device=dev)
     fill_gemm_bf16(X, G.X_TENSOR + rank, G.GEMM_SEED, 0)
@@ -125,9 +104,9 @@ def main(args, root, helpers):
     torch.cuda.synchronize()
 
     h = AgGemm(rank, N, dev, torch_allgather(None, dev), {"timeout_ms": 60000} if shared else None)
-    if args.ag_order >= 0:
+    if getattr(args, "ag_order", -1) >= 0:
         h.set_option("order", args.ag_order)
-    if args.ag_grid:
+    if getattr(args, "ag_grid", 0):
         h.set_option("grid", args.ag_grid)
     h.register(cfg.M, cfg.N_r, cfg.K)
     stream = torch.cuda.current_stream(dev)
@@ -157,14 +136,14 @@ def main(args, root, helpers):
         h.forward(X, Wr, Y, stream)
 
     clk = ClockSampler(local)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         fused()
     torch.cuda.synchronize()
     clk.start()
-    ms = b2b(fused, args.steps, 0)
+    ms = b2b(fused, steps, 0)
     clocks = clk.stop()
     h.check()
-    ms_step = max_over_ranks(ms) / args.steps
+    ms_step = max_over_ranks(ms) / steps
     flops = cfg.flops_per_rank()
     value = N * flops / (ms_step * 1e-3) / 1e12
     peak, peak_sus, peak_src = tensor_peaks(root)
@@ -202,9 +181,10 @@ def main(args, root, helpers):
                       "sampled remote rows of the gather buffer bitwise"}
     okt = torch.tensor([1 if (ok and gathered_ok) else 0], device="cpu" if shared else dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    del Yp
 
     # ---- unfused baseline: NCCL all_gather_into_tensor + cuBLAS
-    Wfull = torch.empty((cfg.N, cfg.K), dtype=torch.bfloat16, device=dev)
+    Wfull = torch.empty((cfg.N, cfg.K), dtype=torch.bfloat16, device=dev) if N > 1 else Wr
     Yb = torch.empty_like(Y)
 
     def unfused():
@@ -215,32 +195,35 @@ def main(args, root, helpers):
                 Wfull.copy_(torch.cat(parts).to(dev))
             else:
                 dist.all_gather_into_tensor(Wfull, Wr)
-            torch.matmul(X, Wfull.t(), out=Yb)
-        else:
-            torch.matmul(X, Wr.t(), out=Yb)
+        torch.matmul(X, Wfull.t(), out=Yb)
 
-    ms_b = max_over_ranks(b2b(unfused, args.steps, args.warmup)) / args.steps
-    ms_gemm = max_over_ranks(b2b(lambda: torch.matmul(X, Wr.t() if N == 1 else Wfull.t(),
-                                                      out=Yb), args.steps, 2)) / args.steps
-    # ---- end to end through the public API: X from pinned host memory in, Y back to pinned host
-    Xh = X.cpu().pin_memory()
-    Yh = torch.empty((cfg.M, cfg.N), dtype=torch.bfloat16).pin_memory()
-    Xd = torch.empty_like(X)
-    e2e_steps = max(2, min(args.steps, 5))
+    ms_b = max_over_ranks(b2b(unfused, steps, warmup)) / steps
+    ms_gemm = max_over_ranks(b2b(lambda: torch.matmul(X, Wfull.t(), out=Yb), steps, 2)) / steps
+    e2e = None
+    if with_e2e:
+        # end to end through the public API: X from pinned host memory in, Y back to pinned host
+        Xh = X.cpu().pin_memory()
+        Yh = torch.empty((cfg.M, cfg.N), dtype=torch.bfloat16).pin_memory()
+        Xd = torch.empty_like(X)
+        e2e_steps = max(2, min(steps, 5))
 
-    def e2e_step():
-        Xd.copy_(Xh, non_blocking=True)
-        h.forward(Xd, Wr, Y, stream)
-        Yh.copy_(Y, non_blocking=True)
-    ms_e2e = max_over_ranks(b2b(e2e_step, e2e_steps, 1)) / e2e_steps
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            h.forward(Xd, Wr, Y, stream)
+            Yh.copy_(Y, non_blocking=True)
+        ms_e2e = max_over_ranks(b2b(e2e_step, e2e_steps, 1)) / e2e_steps
+        e2e = {"value": N * flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": cfg.M * cfg.K * 2, "d2h_bytes_per_step": cfg.M * cfg.N * 2,
+               "ms_per_step": ms_e2e,
+               "api": "ag_gemm_forward with X copied from pinned host and Y copied back each step"}
     cpu = None
-    if not args.no_cpu and rank == 0:
+    if with_cpu and rank == 0:
         v, cores, sample = oracle_sample(cfg, 0, min(args.cpu_seconds, 10.0))
         cpu = dict({"value": v / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                     "sample": sample}, **host_cpu())
     line = {
         "metric": METRIC_AG, "value": value, "unit": "TFLOP/s", "n_gpus": N,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-based bf16-exact operands, synth/gemm_gen.py)",
         "config": {"workload": workload_desc(cfg), "M": cfg.M, "N": cfg.N, "K": cfg.K,
@@ -253,25 +236,60 @@ def main(args, root, helpers):
                      "frac_vs_sustained": achieved / peak_sus,
                      "flops_per_launch": flops, "traffic": None},
         "cpu_baseline": cpu,
-        "e2e": {"value": N * flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
-                "h2d_bytes_per_step": cfg.M * cfg.K * 2, "d2h_bytes_per_step": cfg.M * cfg.N * 2,
-                "ms_per_step": ms_e2e,
-                "api": "ag_gemm_forward with X copied from pinned host and Y copied back each step"},
+        "e2e": e2e,
         "unfused": {"ms_per_step": ms_b, "what": ("NCCL all_gather_into_tensor + torch.matmul "
                                                  "(cuBLAS)" if N > 1 else "torch.matmul (cuBLAS)"),
                     "tflops": N * flops / (ms_b * 1e-3) / 1e12, "fused_speedup": ms_b / ms_step,
                     "cublas_gemm_only_ms": ms_gemm},
         "parity": parity, "parity_all_ranks": bool(okt.item()),
-        "clocks": clocks, "gpu_launches": args.steps,
+        "clocks": clocks, "gpu_launches": steps,
     }
+    h.destroy()
+    del X, Wr, Y, Yb, Wfull
+    torch.cuda.empty_cache()
+    return line
+
+
+def main(args, root, helpers):
+    import torch
+    import torch.distributed as dist
+
+    ClockSampler, host_cpu, dist_env = helpers["ClockSampler"], helpers["host_cpu"], helpers["dist_env"]
+    if args.impl == "reference":
+        return run_reference(args, root, host_cpu)
+    rank, world, local = dist_env()
+    N = world
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    shared = os.environ.get("EMBA2A_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            import socket
+            s = socket.socket()
+            s.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+            s.close()
+        if shared:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    line = measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, args.ag_config,
+                   args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)
+    if shared:
+        line["test_mode"] = "EMBA2A_SHARED_GPU=1: all ranks on one GPU; not a bench value"
     if rank == 0:
         s = json.dumps(line)
         print(s, flush=True)
         if args.out:
             with open(args.out, "a") as f:
                 f.write(s + "\n")
-    h.destroy()
+    ok = line["parity_all_ranks"]
     dist.barrier()
     dist.destroy_process_group()
-    if not okt.item():
+    if not ok:
         raise SystemExit("ag_gemm parity check FAILED")
