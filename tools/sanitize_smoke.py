@@ -68,4 +68,32 @@ for seed, (opts, pooling) in enumerate(cases):
             assert np.array_equal(a_, b_), ("backward", opts, pooling)
     g.destroy()
     n += 1
-print(f"sanitize_smoke: {n} cases OK (W={args.W}), forward + backward")
+# f4: the fused AllGather + GEMM (TMA, mbarriers, tcgen05 MMA/TMEM, communication warps), exact
+# ints -> Y is the oracle's sum rounded once to bf16, bitwise; BN = 256 and BN = 128 shapes
+from oracle import ag_gemm as OAG  # noqa: E402
+from synth import gemm_gen as GG  # noqa: E402
+from synth.device import fill_gemm_bf16  # noqa: E402
+from paper_2305_06942_b200 import AgGemmLoopback  # noqa: E402
+for (M, Nr, K) in ((256, 256, 192), (128, 384, 128)):
+    gc = GG.GemmConfig("san", args.W, M, Nr, K, 1)
+    grp = AgGemmLoopback(args.W, dev, {"timeout_ms": 120000, "local_copy": 1})
+    grp.register(M, Nr, K)
+    ops = []
+    for r in range(args.W):
+        X = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+        Wr = torch.empty((Nr, K), dtype=torch.bfloat16, device=dev)
+        fill_gemm_bf16(X, GG.X_TENSOR + r, GG.GEMM_SEED, 1)
+        fill_gemm_bf16(Wr, GG.W_TENSOR + r, GG.GEMM_SEED, 1)
+        ops.append((X, Wr))
+    for _ in range(2):
+        outs = grp.forward([o[0] for o in ops], [o[1] for o in ops])
+    shards = [GG.rank_inputs(gc, s)[1] for s in range(args.W)]
+    for r in range(args.W):
+        Wf, Yref = OAG.ag_gemm(GG.rank_inputs(gc, r)[0], shards)
+        assert np.array_equal(outs[r][0].view(torch.int16).cpu().numpy().view(np.uint16),
+                              OAG.bf16_rne_bits(Yref)), ("ag_gemm", M, Nr, K, r)
+        assert np.array_equal(outs[r][1].view(torch.int16).cpu().numpy().view(np.uint16),
+                              GG.to_bf16_bits_exact(Wf)), ("ag_gemm gathered", r)
+    grp.destroy()
+    n += 1
+print(f"sanitize_smoke: {n} cases OK (W={args.W}), forward + backward + AllGather+GEMM")
