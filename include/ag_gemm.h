@@ -19,7 +19,8 @@
  * NVLink (zero-copy PUT), in chunks of one GEMM N-tile, destinations staggered
  * r+1, r+2, ... (comm-aware order); the last piece of a chunk fences at system scope and
  * stores the epoch into the destination's per-(source, chunk) ready flag (sliceRdy).
- * Its GEMM warps (TMA producer, tcgen05 MMA issuer, TMEM epilogue) take output tiles in the
+ * Its GEMM warps (TMA producer, tcgen05 MMA issuer, TMEM epilogue; by default a CTA pair per
+ * 256 x BN tile with tcgen05.mma.cta_group::2) take output tiles in the
  * order local shard first, then sources r-1, r-2, ... -- the order the peers' chunks arrive --
  * and the TMA producer waits (ld.acquire.sys) for exactly the chunk a tile's B operand needs.
  *
@@ -88,12 +89,15 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
  *   "piece_kb"    bytes per communication piece, in KiB, power of two 4..1024 (default 64)
  *   "timeout_ms"  bound on every device-side wait (default 10000)
  *   "comm"        0: skip the communication warps (test mode: flags are then never set and a
- *                 remote tile times out) -- default 1 */
+ *                 remote tile times out) -- default 1
+ *   "pair"        1: a cluster of two CTAs (one TPC) per 256 x BN tile, tcgen05.mma.cta_group::2,
+ *                 each CTA staging its 128 A rows and half of the B rows (default; used when
+ *                 M % 256 == 0); 0: one CTA per 128 x BN tile (cta_group::1) */
 int ag_gemm_set_option(ag_gemm_t* h, const char* key, int64_t value);
 int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* value);
 
-/* Derived values: "tiles" (output tiles per forward), "grid", "bn" (N-tile), "chunks" (per
- * source), "pieces" (per chunk), "epoch", "shared_gpu", "smem_bytes". */
+/* Derived values: "tiles" (output tiles per forward), "grid", "pair" (CTA pairs in use), "bn"
+ * (N-tile), "chunks" (per source), "pieces" (per chunk), "epoch", "shared_gpu", "smem_bytes". */
 int ag_gemm_query(const ag_gemm_t* h, const char* key, int64_t* value);
 
 /* Copy this rank's ready flags [W][chunks] (u32 epoch stamps) into out (capacity words). */

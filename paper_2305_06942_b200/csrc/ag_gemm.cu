@@ -40,7 +40,6 @@ constexpr int kMaxW = AG_GEMM_MAX_WORLD;
 constexpr int BM = 128;          // tile rows (UMMA M, one TMEM lane per row)
 constexpr int BK = 64;           // K per stage: 64 bf16 = 128 B rows (SWIZZLE_128B atom)
 constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
-constexpr int kStages = 4;
 constexpr int kThreads = 384;
 constexpr int kCommWarp0 = 8, kCommThreads = 128;
 constexpr int kEpiWarp0 = 4;
@@ -172,21 +171,36 @@ __device__ __forceinline__ unsigned long long smem_desc(unsigned addr) {
 }
 // Instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1, both
 // K-major (bits 15, 16 = 0), N >> 3 at [17,23), M >> 4 at [24,29).
-template <int BN>
+template <int UM, int UN>
 __device__ __forceinline__ unsigned instr_desc() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(BN >> 3) << 17) |
-         ((unsigned)(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(UN >> 3) << 17) |
+         ((unsigned)(UM >> 4) << 24);
 }
+template <bool PAIR>
 __device__ __forceinline__ void mma_bf16(unsigned tmem_d, unsigned long long a,
                                          unsigned long long b, unsigned idesc, unsigned acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+  if (PAIR)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
 }
+// MMA completion -> mbarrier: one CTA, or (CTA pair) the barrier at the same offset in both CTAs
+template <bool PAIR>
 __device__ __forceinline__ void mma_commit(unsigned bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-               ::"r"(bar) : "memory");
+  if (PAIR)
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n\t}" ::"r"(bar) : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(bar) : "memory");
 }
 // 32 consecutive fp32 columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
@@ -200,6 +214,35 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// clusters (CTA pair) ------------------------------------------------------------------------
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the shared::cluster address of `addr` (a shared::cta offset) in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned mapa(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// TMA load into this CTA's shared memory whose completion (bytes) is counted on the pair
+// leader's mbarrier (cta_group::2: the leader's MMA reads both CTAs' stages)
+__device__ __forceinline__ void tma_load_2d_pair(unsigned dst, const CUtensorMap* map,
+                                                 unsigned leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(leader_bar) : "memory");
 }
 
 // ------------------------------------------------------------------------------ tile order
@@ -221,24 +264,42 @@ __device__ __forceinline__ Tile tile_of(const Params& P, int t) {
   return x;
 }
 
+// Per-configuration constants.  PAIR: a cluster of two CTAs (one per SM of a TPC) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2: each CTA stages its own 128 rows of A and half of
+// the tile's B rows (BN/2), the leader issues M = 256 MMAs reading both CTAs' stages, and each
+// CTA's TMEM receives its 128 rows x BN accumulator.  Half the B bytes per SM, so more stages.
+template <int BN, bool PAIR, int NSTG = 0>
+struct Cfg {
+  static constexpr int kBRows = PAIR ? BN / 2 : BN;
+  static constexpr unsigned kABytes = BM * BK * 2;
+  static constexpr unsigned kBBytes = kBRows * BK * 2;
+  static constexpr int kStages = NSTG ? NSTG : (PAIR ? (BN == 256 ? 6 : 8) : 4);
+  static constexpr int kUM = PAIR ? 2 * BM : BM;
+  static constexpr unsigned kTmemCols = 2 * BN;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) +
+                                  8 * (2 * kStages + 4) + 16;
+};
+
 // ---------------------------------------------------------------------------------- kernel
-template <int BN>
+template <int BN, bool PAIR, int NSTG = 0>
 __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_constant__ Params P) {
-  constexpr unsigned kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
-  constexpr unsigned kTmemCols = 2 * BN;
+  using C = Cfg<BN, PAIR, NSTG>;
+  constexpr int NS = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sa = smem;
-  unsigned char* sb = smem + kStages * kABytes;
-  unsigned long long* bars = (unsigned long long*)(sb + kStages * kBBytes);
-  // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
-  unsigned* tmem_slot = (unsigned*)(bars + 2 * kStages + 4);
+  unsigned char* sb = smem + NS * C::kABytes;
+  unsigned long long* bars = (unsigned long long*)(sb + NS * C::kBBytes);
+  // bars: full[NS], empty[NS], tfull[2], tempty[2]
+  unsigned* tmem_slot = (unsigned*)(bars + 2 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned crank = PAIR ? cluster_ctarank() : 0u;     // 0 = the pair's leader
+  const bool leader = crank == 0;
   const unsigned bar0 = smem_u32(bars);
   auto full_bar = [&](int i) { return bar0 + 8u * i; };
-  auto empty_bar = [&](int i) { return bar0 + 8u * (kStages + i); };
-  auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * kStages + i); };
-  auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * kStages + 2 + i); };
+  auto empty_bar = [&](int i) { return bar0 + 8u * (NS + i); };
+  auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * NS + i); };
+  auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * NS + 2 + i); };
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&P.tmA);
@@ -246,20 +307,26 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
     prefetch_map(&P.tmB_g);
   }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(full_bar(i), 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full_bar(i), 1);   // pair: the leader's expect_tx covers both CTAs' bytes
       mbar_init(empty_bar(i), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull_bar(i), 1);
-      mbar_init(tempty_bar(i), 4);     // one arrival per epilogue warp
+      mbar_init(tempty_bar(i), PAIR ? 8 : 4);   // one arrival per epilogue warp (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tmem_slot)), "r"(kTmemCols) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(C::kTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(C::kTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   // this forward started: our previous forward (same stream) has completed, so every peer may
   // overwrite the gather half it used (DESIGN.md Sec 14 buffer reuse)
@@ -267,10 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
     for (int q = 0; q < P.W; ++q)
       if (q != P.rank) red_release_sys_add(P.credit_out[q], 1ull);
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const unsigned tmem_base = *tmem_slot;
   const int ntiles = P.W * P.tiles_m * P.tiles_n;
+  const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // cluster / CTA index
+  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0) {
     // ============================== TMA producer ==============================
@@ -279,10 +348,11 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
       unsigned phase = 0;
       int ready_s = -1, ready_n = -1;
       bool ok = true;
-      for (int t = blockIdx.x; t < ntiles && ok; t += gridDim.x) {
+      const unsigned lbar0 = PAIR ? mapa(full_bar(0), 0) : full_bar(0);   // leader's full[0]
+      for (int t = unit; t < ntiles && ok; t += nunits) {
         const Tile x = tile_of(P, t);
         const CUtensorMap* mb = &P.tmB_local;
-        int brow = x.n * BN;
+        int brow = x.n * BN + (int)crank * C::kBRows;
         if (x.s != P.rank) {
           mb = &P.tmB_g;
           brow += x.s * P.N_r;
@@ -305,24 +375,38 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
             ready_n = x.n;
           }
         }
+        const int arow = x.m * C::kUM + (int)crank * BM;
         for (int kb = 0; kb < P.k_blocks && ok; ++kb) {
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, P)) { ok = false; break; }
-          mbar_expect_tx(full_bar(stage), kABytes + kBBytes);
-          tma_load_2d(smem_u32(sa + stage * kABytes), &P.tmA, full_bar(stage), kb * BK, x.m * BM);
-          tma_load_2d(smem_u32(sb + stage * kBBytes), mb, full_bar(stage), kb * BK, brow);
-          if (++stage == kStages) { stage = 0; phase ^= 1u; }
+          const unsigned da = smem_u32(sa + stage * C::kABytes);
+          const unsigned db = smem_u32(sb + stage * C::kBBytes);
+          if (PAIR) {
+            // the peer's bytes may land on the leader's barrier before the leader's expect_tx
+            // (a transiently negative tx-count); the phase cannot complete without the leader's
+            // arrival, and the peer refills a stage only after the MMA freed it (its own empty
+            // barrier, multicast commit).  (A remote arrive per stage was a MEMBAR.GPU each.)
+            const unsigned lb = lbar0 + 8u * stage;
+            if (leader) mbar_expect_tx(full_bar(stage), 2 * (C::kABytes + C::kBBytes));
+            tma_load_2d_pair(da, &P.tmA, lb, kb * BK, arow);
+            tma_load_2d_pair(db, mb, lb, kb * BK, brow);
+          } else {
+            mbar_expect_tx(full_bar(stage), C::kABytes + C::kBBytes);
+            tma_load_2d(da, &P.tmA, full_bar(stage), kb * BK, arow);
+            tma_load_2d(db, mb, full_bar(stage), kb * BK, brow);
+          }
+          if (++stage == NS) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
-    // ============================== MMA issuer ================================
-    if (lane == 0) {
-      const unsigned idesc = instr_desc<BN>();
+    // ============================== MMA issuer (the pair's leader) ============
+    if (lane == 0 && leader) {
+      const unsigned idesc = instr_desc<C::kUM, BN>();
       int stage = 0;
       unsigned phase = 0;
       int it = 0;
       bool ok = true;
-      for (int t = blockIdx.x; t < ntiles && ok; t += gridDim.x, ++it) {
+      for (int t = unit; t < ntiles && ok; t += nunits, ++it) {
         const int as = it & 1;
         const unsigned aph = (unsigned)(it >> 1) & 1u;
         if (!mbar_wait(tempty_bar(as), aph ^ 1u, P)) break;
@@ -331,29 +415,30 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
         for (int kb = 0; kb < P.k_blocks; ++kb) {
           if (!mbar_wait(full_bar(stage), phase, P)) { ok = false; break; }
           tc_fence_after();
-          const unsigned a0 = smem_u32(sa + stage * kABytes);
-          const unsigned b0 = smem_u32(sb + stage * kBBytes);
+          const unsigned a0 = smem_u32(sa + stage * C::kABytes);
+          const unsigned b0 = smem_u32(sb + stage * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)   // +32 B along K inside the 128-B swizzled row
-            mma_bf16(dacc, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2), idesc,
-                     (kb | k) != 0);
-          mma_commit(empty_bar(stage));       // frees the stage once these MMAs have read it
-          if (++stage == kStages) { stage = 0; phase ^= 1u; }
+            mma_bf16<PAIR>(dacc, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2), idesc,
+                           (kb | k) != 0);
+          mma_commit<PAIR>(empty_bar(stage));   // frees the stage (in both CTAs of a pair)
+          if (++stage == NS) { stage = 0; phase ^= 1u; }
         }
-        mma_commit(tfull_bar(as));            // accumulator complete -> epilogue
+        mma_commit<PAIR>(tfull_bar(as));        // accumulator complete -> epilogue(s)
       }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     // ============================== epilogue ==================================
     const int q = warp & 3;                   // TMEM lanes 32q..32q+31 = tile rows
+    const unsigned lt0 = PAIR ? mapa(tempty_bar(0), 0) : tempty_bar(0);
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int t = unit; t < ntiles; t += nunits, ++it) {
       const Tile x = tile_of(P, t);
       const int as = it & 1;
       const unsigned aph = (unsigned)(it >> 1) & 1u;
       if (!mbar_wait(tfull_bar(as), aph, P)) break;
       tc_fence_after();
-      const long long row = (long long)x.m * BM + q * 32 + lane;
+      const long long row = (long long)x.m * C::kUM + (long long)crank * BM + q * 32 + lane;
       const long long col0 = (long long)x.s * P.N_r + (long long)x.n * BN;
       const unsigned taddr = tmem_base + ((unsigned)(q * 32) << 16) + (unsigned)(as * BN);
 #pragma unroll 1
@@ -381,7 +466,10 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(as));
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(lt0 + 8u * as);   // the leader's MMA reuses both halves
+        else mbar_arrive(tempty_bar(as));
+      }
     }
   } else if (warp >= kCommWarp0 && P.comm) {
     // ============================== communication =============================
@@ -453,17 +541,16 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();   // both CTAs done with TMEM and stages
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::kTmemCols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::kTmemCols) : "memory");
   }
-}
-
-template <int BN>
-constexpr size_t smem_bytes() {
-  return 1024 + (size_t)kStages * (BM * BK * 2 + BN * BK * 2) + 8 * (2 * kStages + 4) + 16;
 }
 
 }  // namespace aggemm
@@ -513,7 +600,7 @@ struct ag_gemm {
   int* h_err = nullptr;
   int* d_err = nullptr;
   int64_t opt_grid = 0, local_copy = 0, order = 0, group_m = 16, piece_kb = 64,
-          timeout_ms = 10000, comm = 1;
+          timeout_ms = 10000, comm = 1, pair = 1, stages = 6;
 };
 
 namespace {
@@ -583,6 +670,46 @@ int make_map(ag_gemm* h, CUtensorMap* m, const void* base, int64_t rows, int64_t
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(h, 1, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return 0;
+}
+
+template <int BN, bool PAIR, int NSTG = 0>
+cudaError_t set_smem_attr() {
+  return cudaFuncSetAttribute(ag_gemm_kernel<BN, PAIR, NSTG>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)Cfg<BN, PAIR, NSTG>::kSmem);
+}
+
+// CTA pairs (cta_group::2) need M % 256 == 0 and an even grid; option "pair" 0 forces single CTAs
+bool use_pair(const ag_gemm* h) { return h->pair && h->M % 256 == 0; }
+
+int64_t grid_of(const ag_gemm* h) {
+  const bool pair = use_pair(h);
+  const int64_t tiles = (int64_t)h->W * (h->M / (pair ? 256 : 128)) * h->chunks;
+  int64_t g = h->opt_grid > 0 ? h->opt_grid : (h->shared_gpu ? h->sms / h->W : h->sms);
+  if (pair) {
+    g = std::max<int64_t>(1, std::min<int64_t>(g / 2, tiles)) * 2;   // clusters of two CTAs
+  } else {
+    g = std::max<int64_t>(1, std::min<int64_t>(g, tiles));
+  }
+  return g;
+}
+
+template <int BN, bool PAIR, int NSTG = 0>
+cudaError_t launch(const Params& P, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<BN, PAIR, NSTG>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ag_gemm_kernel<BN, PAIR, NSTG>, P);
 }
 
 void release(ag_gemm* h) {
@@ -716,13 +843,11 @@ int ag_gemm_register(ag_gemm_t* h, int64_t M, int64_t n_local, int64_t K, int ou
       h->peer_base[q] = (char*)p;
     }
   }
-  const size_t smem = h->BN == 256 ? smem_bytes<256>() : smem_bytes<128>();
-  if (h->BN == 256)
-    AG_TRY(h, cudaFuncSetAttribute(ag_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-  else
-    AG_TRY(h, cudaFuncSetAttribute(ag_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  AG_TRY(h, (set_smem_attr<256, false>()));
+  AG_TRY(h, (set_smem_attr<128, false>()));
+  AG_TRY(h, (set_smem_attr<256, true>()));
+  AG_TRY(h, (set_smem_attr<128, true>()));
+  AG_TRY(h, (set_smem_attr<256, true, 7>()));
   h->registered = true;
   return 0;
 }
@@ -741,10 +866,12 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
   const int half = (int)(e & 1u);
   Params P;
   memset(&P, 0, sizeof(P));
+  const bool pair = use_pair(h);
+  const int brows = pair ? h->BN / 2 : h->BN;   // B rows one CTA stages per tile
   rc = make_map(h, &P.tmA, X, h->M, h->K, BM);
-  if (!rc) rc = make_map(h, &P.tmB_local, w_local, h->N_r, h->K, h->BN);
+  if (!rc) rc = make_map(h, &P.tmB_local, w_local, h->N_r, h->K, brows);
   char* my_half = h->region + h->flag_bytes + h->credit_bytes + (size_t)half * h->half_bytes;
-  if (!rc) rc = make_map(h, &P.tmB_g, my_half, (int64_t)h->W * h->N_r, h->K, h->BN);
+  if (!rc) rc = make_map(h, &P.tmB_g, my_half, (int64_t)h->W * h->N_r, h->K, brows);
   if (rc) return rc;
   P.Y = Y;
   P.ldy = (long long)h->W * h->N_r;
@@ -754,7 +881,7 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
   P.K = (int)h->K;
   P.W = h->W;
   P.rank = h->rank;
-  P.tiles_m = (int)(h->M / BM);
+  P.tiles_m = (int)(h->M / (pair ? 2 * BM : BM));
   P.tiles_n = h->chunks;
   P.k_blocks = (int)(h->K / BK);
   P.group_m = (int)std::max<int64_t>(1, h->group_m);
@@ -780,14 +907,14 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
   P.local_copy = (int)h->local_copy;
   P.err = h->d_err;
   P.timeout_ns = h->timeout_ms * 1000000ll;
-  const int ntiles = h->W * P.tiles_m * P.tiles_n;
-  int grid = h->opt_grid > 0 ? (int)h->opt_grid : (h->shared_gpu ? h->sms / h->W : h->sms);
-  grid = std::max(1, std::min(grid, ntiles));
+  const int grid = (int)grid_of(h);
   cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t le;
   if (h->BN == 256)
-    ag_gemm_kernel<256><<<grid, kThreads, smem_bytes<256>(), st>>>(P);
-  else
-    ag_gemm_kernel<128><<<grid, kThreads, smem_bytes<128>(), st>>>(P);
+    le = pair ? (h->stages == 7 ? launch<256, true, 7>(P, grid, st) : launch<256, true>(P, grid, st))
+              : launch<256, false>(P, grid, st);
+  else le = pair ? launch<128, true>(P, grid, st) : launch<128, false>(P, grid, st);
+  if (le != cudaSuccess) return fail(h, 3, "launch: %s", cudaGetErrorString(le));
   cudaError_t ce = cudaGetLastError();
   if (ce != cudaSuccess) return fail(h, 3, "launch: %s", cudaGetErrorString(ce));
   h->epoch = e;
@@ -809,6 +936,8 @@ int ag_gemm_set_option(ag_gemm_t* h, const char* key, int64_t v) {
   }
   else if (k == "timeout_ms") { if (v < 1) return fail(h, 1, "timeout_ms >= 1"); h->timeout_ms = v; }
   else if (k == "comm") { if (v != 0 && v != 1) return fail(h, 1, "comm 0/1"); h->comm = v; }
+  else if (k == "pair") { if (v != 0 && v != 1) return fail(h, 1, "pair 0/1"); h->pair = v; }
+  else if (k == "stages") { if (v != 6 && v != 7) return fail(h, 1, "stages 6/7"); h->stages = v; }
   else return fail(h, 1, "unknown option '%s'", key);
   return 0;
 }
@@ -823,6 +952,8 @@ int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* v) {
   else if (k == "piece_kb") *v = h->piece_kb;
   else if (k == "timeout_ms") *v = h->timeout_ms;
   else if (k == "comm") *v = h->comm;
+  else if (k == "pair") *v = h->pair;
+  else if (k == "stages") *v = h->stages;
   else return 1;
   return 0;
 }
@@ -830,18 +961,21 @@ int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* v) {
 int ag_gemm_query(const ag_gemm_t* h, const char* key, int64_t* v) {
   if (!h || !key || !v) return 1;
   std::string k(key);
-  const int64_t tiles = h->registered ? (int64_t)h->W * (h->M / BM) * h->chunks : 0;
+  const bool pair = h->registered && use_pair(h);
+  const int64_t tiles = h->registered ? (int64_t)h->W * (h->M / (pair ? 256 : 128)) * h->chunks : 0;
   if (k == "tiles") *v = tiles;
-  else if (k == "grid") {
-    int64_t g = h->opt_grid > 0 ? h->opt_grid : (h->shared_gpu ? h->sms / h->W : h->sms);
-    *v = std::max<int64_t>(1, std::min<int64_t>(g, std::max<int64_t>(tiles, 1)));
-  }
+  else if (k == "grid") *v = h->registered ? grid_of(h) : 0;
+  else if (k == "pair") *v = pair ? 1 : 0;
   else if (k == "bn") *v = h->BN;
   else if (k == "chunks") *v = h->chunks;
   else if (k == "pieces") *v = h->pieces;
   else if (k == "epoch") *v = h->epoch;
   else if (k == "shared_gpu") *v = h->shared_gpu ? 1 : 0;
-  else if (k == "smem_bytes") *v = (int64_t)(h->BN == 256 ? smem_bytes<256>() : smem_bytes<128>());
+  else if (k == "smem_bytes")
+    *v = (int64_t)(h->BN == 256 ? (pair ? (h->stages == 7 ? Cfg<256, true, 7>::kSmem
+                                                         : Cfg<256, true>::kSmem)
+                                        : Cfg<256, false>::kSmem)
+                                : (pair ? Cfg<128, true>::kSmem : Cfg<128, false>::kSmem));
   else return 1;
   return 0;
 }

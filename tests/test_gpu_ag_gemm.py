@@ -201,3 +201,28 @@ def test_full_size_sampled_entries(name, W):
                 np.testing.assert_array_equal(row, ref)
     finally:
         grp.destroy()
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("M,N_r,K,W", [(256, 256, 512, 1), (512, 384, 256, 1), (768, 512, 320, 2),
+                                       (256, 128, 128, 4)])
+def test_cta_pair_and_single_cta_paths(pair, M, N_r, K, W):
+    """tcgen05.mma.cta_group::2 (a CTA pair per 256 x BN tile, each CTA staging half of B) and
+    the single-CTA path give the same bitwise result; the query reports which one ran."""
+    flags = run_loopback(cfg_of(W, M, N_r, K), opts={"pair": pair, "grid": 6})
+    assert flags.shape == (W, N_r // (256 if N_r % 256 == 0 else 128))
+
+
+def test_pair_query_and_odd_grid():
+    from paper_2305_06942_b200 import AgGemm, LocalGroup
+    h = AgGemm(0, 1, dev(), LocalGroup(1).allgather_for(0), {"grid": 7})
+    try:
+        h.register(512, 1024, 128)                                # 2 x 4 pair tiles
+        assert h.query("pair") == 1 and h.query("grid") == 6      # even: clusters of two
+        h.set_option("pair", 0)
+        assert h.query("pair") == 0 and h.query("grid") == 7
+        h.register(384, 256, 128)                                 # M % 256 != 0: single CTAs
+        h.set_option("pair", 1)
+        assert h.query("pair") == 0
+    finally:
+        h.destroy()
