@@ -264,9 +264,12 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *                  its indices from global memory
  *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
  *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
- *   "sort_mode"    backward plan's radix passes: 0 auto (default: one kernel per pass with
+ *   "sort_mode"    backward plan's radix passes: 0 auto (default: one kernel per 8-bit pass with
  *                  look-back while the tiles fit one wave, else three kernels per pass,
- *                  reduce-then-scan), 1 always one kernel, 2 always three (results identical)
+ *                  reduce-then-scan), 1 always one kernel, 2 always three, 3 the segmented plan
+ *                  (each table's lookups sorted by row bits only: 2 passes of <= 11-bit digits,
+ *                  tiles aligned to tables; needs rows <= 2^22 and T <= 256, else as 0) --
+ *                  results identical in every mode
  *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 128] (default 128;
  *                  the kernel is compiled with __launch_bounds__(128))
  *   "bwd_share"    divide the backward's persistent grid by this (default 1): W virtual ranks on

@@ -514,6 +514,323 @@ __global__ void __launch_bounds__(kSortThreads) bwd_downsweep_kernel(const PassP
   }
 }
 
+// ------------------------------------------------------------------ segmented sort plan
+// The input is table-major (table t's lookups are offsets[t*B] .. offsets[(t+1)*B]) and the sort
+// is stable, so sorting every table's segment by ROW alone gives exactly the (table, row) order
+// of the plain plan while the digits cover only the row bits: 2 passes of <= 11-bit digits for
+// tables of up to 4M rows (DLRM-small: 23-bit keys = 3 plain passes).  Digit counts are kept per
+// (table, digit); tiles never straddle tables, and the look-back runs over the earlier tiles of
+// the same table only.
+
+// Keys/payloads as in bwd_keygen_kernel, plus the per-(table, digit) counts of both passes.  A
+// CTA's bag groups are contiguous (one grid-stride step when TB <= 64 x grid), so their tables
+// fall in a window of two: counted in shared memory; anything outside goes to global atomics.
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(256) bwd_keygen_seg_kernel(const SortParams S) {
+  constexpr int BPW = 8;
+  extern __shared__ unsigned h[];                // [2 window tables][2 passes][NB]
+  const int NB = 1 << S.seg_db;
+  const int nwin = 4 * NB;
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) h[i] = 0u;
+  pdl_wait();     // the caller's indices/offsets and the previous plan's passes are complete
+  pdl_trigger();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.lbg_words;
+       i += (long long)gridDim.x * blockDim.x)
+    S.lbg[i] = 0u;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.shist_words;
+       i += (long long)gridDim.x * blockDim.x)
+    S.shist_clear[i] = 0u;                       // the next plan's counts and tile tickets
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const unsigned m0 = (1u << S.seg_db) - 1u;
+  const unsigned m1 = S.rbits > S.seg_db ? (1u << (S.rbits - S.seg_db)) - 1u : 0u;
+  const long long ngroups = (S.TB + BPW - 1) / BPW;
+  const long long nwt = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long tw = ((long long)blockIdx.x * (blockDim.x >> 5) * BPW) / S.B;   // window base
+  for (long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; grp < ngroups;
+       grp += nwt) {
+    const long long b0 = grp * BPW;
+    const int nb = (S.TB - b0) < BPW ? (int)(S.TB - b0) : BPW;
+    const int my_off = lane < nb ? S.offsets[b0 + lane] : 0x7fffffff;
+    const int lo = __shfl_sync(kFull, my_off, 0);
+    const int hi = S.offsets[b0 + nb];
+    constexpr int UNROLL = 8;
+    for (int base0 = lo; base0 < hi; base0 += 32 * UNROLL) {
+      int ix[UNROLL];
+      float wv[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int p = base0 + 32 * u + lane;
+        ix[u] = p < hi ? S.indices[p] : 0;
+        if (WEIGHTED) wv[u] = p < hi ? S.weights[p] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int p = base0 + 32 * u + lane;
+        if (base0 + 32 * u >= hi) break;            // warp-uniform
+        int i = 0;
+#pragma unroll
+        for (int step = BPW / 2; step >= 1; step >>= 1) {
+          const int v = __shfl_sync(kFull, my_off, i + step);
+          if (i + step < nb && v <= p) i += step;
+        }
+        if (p < hi) {
+          const long long bag = b0 + i;
+          const unsigned t = (unsigned)(bag / S.B);
+          const unsigned row = (unsigned)ix[u];
+          S.keys[p] = (t << S.rbits) | row;
+          S.bags[p] = (int)bag;
+          if (WEIGHTED) S.wts[p] = wv[u];
+          const unsigned d0 = row & m0, d1 = (row >> S.seg_db) & m1;
+          const long long wl = (long long)t - tw;
+          if (wl == 0 || wl == 1) {
+            atomicAdd(&h[((int)wl * 2 + 0) * NB + d0], 1u);
+            atomicAdd(&h[((int)wl * 2 + 1) * NB + d1], 1u);
+          } else {
+            atomicAdd(S.shist + ((size_t)t) * NB + d0, 1u);
+            atomicAdd(S.shist + ((size_t)S.T + t) * NB + d1, 1u);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
+    const unsigned c = h[i];
+    if (!c) continue;
+    const long long t = tw + i / (2 * NB);
+    const int p = (i / NB) & 1, d = i % NB;
+    if (t < S.T) atomicAdd(S.shist + ((size_t)p * S.T + t) * NB + d, c);
+  }
+}
+
+// Exclusive scan over NB = 256 * DPT values, DPT consecutive values per thread: returns each of
+// this thread's exclusive prefixes in x[] (in place) and the block total.
+template <int DPT>
+__device__ __forceinline__ unsigned block_excl_scan_dpt(unsigned (&x)[DPT], unsigned* s_warp) {
+  unsigned tot = 0;
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    const unsigned v = x[k];
+    x[k] = tot;
+    tot += v;
+  }
+  const unsigned base = block_excl_scan256(tot, s_warp);
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) x[k] += base;
+  __syncthreads();                          // s_warp reused by the caller's next scan
+  return base + tot;
+}
+
+// One stable LSD pass over the row digit of every table segment (onesweep, tiles aligned to
+// tables, taken in ticket order).  Same structure as bwd_onesweep_kernel; NB = 2^DB digits,
+// DPT = NB / 256 consecutive digits per thread in the digit-wise steps.
+template <bool WEIGHTS, int DB>
+__global__ void __launch_bounds__(kSortThreads) bwd_onesweep_seg_kernel(const PassParams P) {
+  constexpr int NW = kSortThreads / 32;
+  constexpr int NB = 1 << DB;
+  constexpr int DPT = NB / kSortThreads;
+  static_assert(DPT >= 1 && kSortThreads == 256, "digits per thread");
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(sm);          // [NW][NB]
+  unsigned* s_hist = reinterpret_cast<unsigned*>(sm + (size_t)NW * NB * 2);  // [NB] -> tile start
+  unsigned* s_gofs = s_hist + NB;                                          // [NB]
+  unsigned* s_key = s_gofs + NB;                                           // [tile]
+  int* s_bag = reinterpret_cast<int*>(s_key + kSortTile);
+  float* s_wt = reinterpret_cast<float*>(s_bag + kSortTile);
+  __shared__ unsigned s_warp[NW];
+  __shared__ unsigned s_tile, s_ntiles;
+  __shared__ int s_t;
+  __shared__ unsigned s_tpre[kSortThreads], s_gpre[kSortThreads];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_trigger();
+  for (int i = tid; i < NW * NB / 2; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
+  for (int i = tid; i < NB; i += kSortThreads) s_hist[i] = 0u;
+  pdl_wait();
+  if (tid == 0) s_tile = atomicAdd(P.tile_ctr, 1u);
+  // table map: tiles and look-back groups per table (T <= 256, one table per thread)
+  long long o_t = 0, n_t = 0;
+  unsigned nt = 0, ng = 0;
+  if (tid < P.T) {
+    o_t = P.offsets[(long long)tid * P.B];
+    n_t = P.offsets[(long long)(tid + 1) * P.B] - o_t;
+    nt = (unsigned)((n_t + kSortTile - 1) / kSortTile);
+    ng = (nt + kSegLb - 1) / kSegLb;
+  }
+  const unsigned tpre = block_excl_scan256(nt, s_warp);
+  __syncthreads();
+  const unsigned gpre = block_excl_scan256(ng, s_warp);
+  s_tpre[tid] = tpre;
+  s_gpre[tid] = gpre;
+  if (tid == kSortThreads - 1) s_ntiles = tpre + nt;
+  __syncthreads();
+  const unsigned g = s_tile;
+  if (g >= s_ntiles) return;                 // surplus ticket (the grid is an upper bound)
+  if (tid < P.T && nt > 0 && g >= tpre && g < tpre + nt) s_t = tid;
+  __syncthreads();
+  const int t = s_t;
+  const long long seg0 = P.offsets[(long long)t * P.B];
+  const long long segn = P.offsets[(long long)(t + 1) * P.B] - seg0;
+  const unsigned j = g - s_tpre[t];                    // tile index within the table
+  const unsigned ntt = (unsigned)((segn + kSortTile - 1) / kSortTile);
+  const unsigned ngt = (ntt + kSegLb - 1) / kSegLb;
+  const unsigned J = j / kSegLb, j0 = J * kSegLb;      // look-back group within the table
+  const unsigned gg = s_gpre[t] + J;                   // its global group id
+  const long long start = seg0 + (long long)j * kSortTile;
+  const int len = (segn - (long long)j * kSortTile) < kSortTile
+                      ? (int)(segn - (long long)j * kSortTile) : kSortTile;
+  const int base = w * (32 * kSortItems);
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  unsigned key[kSortItems];
+  int bag[kSortItems];
+  float wt[kSortItems];
+  unsigned short rank[kSortItems];
+  unsigned peers[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int pos = base + i * 32 + lane;
+    const bool valid = pos < len;
+    key[i] = valid ? P.keys_in[start + pos] : 0u;
+    bag[i] = valid ? P.bags_in[start + pos] : 0;
+    if (WEIGHTS) wt[i] = valid ? P.wts_in[start + pos] : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int pos = base + i * 32 + lane;
+    const unsigned d = pos < len ? ((key[i] >> P.shift) & P.dmask) : (unsigned)NB;
+    peers[i] = __match_any_sync(kFull, d);
+    if (d < (unsigned)NB && lane == __ffs(peers[i]) - 1) atomicAdd(&s_hist[d], __popc(peers[i]));
+  }
+  __syncthreads();
+  unsigned run[DPT];
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) run[k] = s_hist[tid * DPT + k];
+  // publish: the tile's stamped words (read by the later tiles of its group) and, unless this is
+  // the table's last group, the group's digit sums + one arrival
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    const unsigned d = tid * DPT + k;
+    st_relaxed_gpu(P.status + (size_t)g * NB + d,
+                   lb_word(P.stall && g == 0 ? P.stamp + 1u : P.stamp, 1, run[k]));
+    if (J + 1 < ngt && run[k]) atomicAdd(P.gsum + (size_t)gg * NB + d, run[k]);
+  }
+  __syncthreads();
+  if (tid == 0 && J + 1 < ngt) {
+    __threadfence();
+    atomicAdd(P.garrive + gg, 1u);
+  }
+  // stable rank of each key within its warp's digit
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int pos = base + i * 32 + lane;
+    const unsigned dd = pos < len ? ((key[i] >> P.shift) & P.dmask) : (unsigned)NB;
+    const unsigned c = dd < (unsigned)NB ? s_cnt[w * NB + dd] : 0u;
+    rank[i] = (unsigned short)(c + __popc(peers[i] & lt_mask));
+    __syncwarp();
+    if (dd < (unsigned)NB && lane == __ffs(peers[i]) - 1)
+      s_cnt[w * NB + dd] = (unsigned short)(c + __popc(peers[i]));
+    __syncwarp();
+  }
+  __syncthreads();
+  // per-warp exclusive offsets of my digits
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    const int d = tid * DPT + k;
+    unsigned acc = 0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) {
+      const unsigned c = s_cnt[ww * NB + d];
+      s_cnt[ww * NB + d] = (unsigned short)acc;
+      acc += c;
+    }
+  }
+  // look-back over the earlier tiles of this table: the words of tiles j0 .. j-1 of its group,
+  // then the sums of its earlier (complete) groups
+  const unsigned want = P.stamp & 0x3fffffffu;
+  const unsigned long long tb = globaltimer();
+  unsigned excl[DPT];
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) excl[k] = 0u;
+  {
+    unsigned long long v[kSegLb - 1][DPT];
+#pragma unroll
+    for (int i = 0; i < kSegLb - 1; ++i)
+#pragma unroll
+      for (int k = 0; k < DPT; ++k)
+        v[i][k] = (j0 + i < j) ? ld_relaxed_gpu(P.status + (size_t)(g - (j - j0 - i)) * NB +
+                                                tid * DPT + k)
+                               : 0ull;
+    // while those are in flight: the table's digit base and the tile's first slot per digit
+    unsigned gb[DPT], ts[DPT];
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) {
+      gb[k] = P.shist[(size_t)t * NB + tid * DPT + k];
+      ts[k] = run[k];
+    }
+    block_excl_scan_dpt<DPT>(gb, s_warp);
+    block_excl_scan_dpt<DPT>(ts, s_warp);
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) s_hist[tid * DPT + k] = ts[k];   // tile start of each digit
+#pragma unroll
+    for (int i = 0; i < kSegLb - 1; ++i) {
+      if (j0 + i >= j) continue;
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) {
+        unsigned long long x = v[i][k];
+        while ((unsigned)(x >> 34) != want || ((unsigned)(x >> 32) & 3u) == 0u) {
+          if (globaltimer() - tb > (unsigned long long)P.timeout_ns) {
+            atomicExch(P.err, 0x4000);
+            break;
+          }
+          x = ld_relaxed_gpu(P.status + (size_t)(g - (j - j0 - i)) * NB + tid * DPT + k);
+        }
+        excl[k] += (unsigned)x;
+      }
+    }
+    if (J > 0) {
+      const unsigned gfirst = s_gpre[t];
+      for (unsigned jj = tid; jj < J; jj += kSortThreads) {
+        while (ld_acquire_gpu_u32(P.garrive + gfirst + jj) < (unsigned)kSegLb)
+          if (globaltimer() - tb > (unsigned long long)P.timeout_ns) {
+            atomicExch(P.err, 0x4000);
+            break;
+          }
+      }
+      __syncthreads();                 // the acquires above order the group sums read below
+      for (unsigned jj = 0; jj < J; ++jj)
+#pragma unroll
+        for (int k = 0; k < DPT; ++k)
+          excl[k] += ld_relaxed_gpu_u32(P.gsum + (size_t)(gfirst + jj) * NB + tid * DPT + k);
+    }
+#pragma unroll
+    for (int k = 0; k < DPT; ++k)
+      s_gofs[tid * DPT + k] = (unsigned)seg0 + gb[k] + excl[k];
+  }
+  __syncthreads();
+  // reorder the tile by digit in shared memory, then write each digit's run out contiguously
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int pos = base + i * 32 + lane;
+    if (pos < len) {
+      const unsigned dd = (key[i] >> P.shift) & P.dmask;
+      const unsigned lp = s_hist[dd] + s_cnt[w * NB + dd] + rank[i];
+      s_key[lp] = key[i];
+      s_bag[lp] = bag[i];
+      if (WEIGHTS) s_wt[lp] = wt[i];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < len; i += kSortThreads) {
+    const unsigned k = s_key[i];
+    const unsigned dd = (k >> P.shift) & P.dmask;
+    const unsigned out = s_gofs[dd] + (unsigned)i - s_hist[dd];
+    P.keys_out[out] = k;
+    P.bags_out[out] = s_bag[i];
+    if (WEIGHTS) P.wts_out[out] = s_wt[i];
+  }
+}
+
 // ------------------------------------------------------------------------- fused backward
 // Per-warp timeline of the backward (the "trace" option; read with emb_a2a_read_trace): record
 // (warp << 40 | event << 32 | payload, %globaltimer).  Events: 20 warp start, 21 exchange done,
@@ -1138,6 +1455,56 @@ cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int 
     const void* fn = passes[p].wts_in ? reinterpret_cast<const void*>(bwd_downsweep_kernel<true>)
                                       : reinterpret_cast<const void*>(bwd_downsweep_kernel<false>);
     if (e == cudaSuccess) e = launch_pdl(fn, (unsigned)ntiles, kSortThreads, 0, st, args);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+size_t seg_sort_smem(int db, bool weights) {
+  const size_t NB = (size_t)1 << db;
+  return (size_t)(kSortThreads / 32) * NB * 2 + 2 * NB * 4 +
+         (size_t)kSortTile * (weights ? 12 : 8);
+}
+
+namespace {
+template <bool W, int DB>
+cudaError_t launch_seg_pass(const PassParams& pp, long long grid, cudaStream_t st) {
+  const void* fn = reinterpret_cast<const void*>(bwd_onesweep_seg_kernel<W, DB>);
+  const size_t sm = seg_sort_smem(DB, W);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  PassParams q = pp;
+  void* args[] = {&q};
+  return launch_pdl(fn, (unsigned)grid, kSortThreads, sm, st, args);
+}
+template <bool W>
+cudaError_t launch_seg_pass_db(const PassParams& pp, int db, long long grid, cudaStream_t st) {
+  switch (db) {
+    case 8: return launch_seg_pass<W, 8>(pp, grid, st);
+    case 9: return launch_seg_pass<W, 9>(pp, grid, st);
+    case 10: return launch_seg_pass<W, 10>(pp, grid, st);
+    case 11: return launch_seg_pass<W, 11>(pp, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+}  // namespace
+
+cudaError_t launch_sort_plan_seg(const SortParams& S, const PassParams* passes, int npasses,
+                                 long long ntiles_max, int grid_keygen, cudaStream_t st) {
+  if (S.TB > 0) {
+    SortParams s = S;
+    void* args[] = {&s};
+    const size_t sm = (size_t)4 * ((size_t)1 << S.seg_db) * 4;
+    const void* fn = S.weights ? reinterpret_cast<const void*>(bwd_keygen_seg_kernel<true>)
+                               : reinterpret_cast<const void*>(bwd_keygen_seg_kernel<false>);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess) e = launch_pdl(fn, (unsigned)grid_keygen, 256, sm, st, args);
+    if (e != cudaSuccess) return e;
+  }
+  for (int p = 0; p < npasses; ++p) {
+    cudaError_t e = passes[p].wts_in
+                        ? launch_seg_pass_db<true>(passes[p], S.seg_db, ntiles_max, st)
+                        : launch_seg_pass_db<false>(passes[p], S.seg_db, ntiles_max, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

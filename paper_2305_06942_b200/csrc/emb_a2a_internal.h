@@ -177,6 +177,7 @@ constexpr int kSortTile = kSortThreads * kSortItems;   // keys per onesweep tile
 constexpr int kMaxPasses = 4;                          // 32-bit keys
 constexpr int kHistWords = kMaxPasses * 256 + kMaxPasses;   // digit counts + tile tickets
 constexpr int kLbGroup = 16;                           // onesweep look-back group (tiles)
+constexpr int kSegLb = 4;                              // segmented plan: look-back group (tiles)
 
 struct SortParams {
   const int* indices;
@@ -192,6 +193,13 @@ struct SortParams {
   unsigned last_mask;          // digit mask of the last pass (the key may end inside a digit)
   unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)
   long long lbg_words;
+  // segmented plan (seg_db > 0): digits are row bits only, counted per (table, digit); the
+  // input is table-major, so each table's lookups are sorted in place of its own segment
+  int seg_db;                  // digit bits of both passes (the last may be narrower)
+  int T;                       // tables (<= 256)
+  unsigned* shist;             // [2 passes][T][1 << seg_db] digit counts (zero at entry)
+  unsigned* shist_clear;       // the other half, zeroed here for the next plan
+  long long shist_words;       // words per half (incl. the 2 tile tickets)
 };
 
 struct PassParams {
@@ -217,6 +225,11 @@ struct PassParams {
   int* err;                    // device error word (look-back timeout -> EMB_A2A_ETIMEOUT)
   long long timeout_ns;
   int stall;                   // debug: tile 0 publishes a stale stamp (tests the timeout)
+  // segmented pass (bwd_onesweep_seg_kernel): tiles never straddle tables
+  const int* offsets;          // the plan's CSR offsets: table t's lookups start at offsets[t*B]
+  long long B;
+  int T;
+  const unsigned* shist;       // this pass's [T][NB] per-table digit counts
 };
 
 // The fused backward (exchange + reduce + update) and the unfused reduce share one kernel.
@@ -256,6 +269,11 @@ struct BwdParams {
 // 2 reduce-then-scan
 cudaError_t launch_sort_plan(const SortParams& S, const PassParams* passes, int npasses,
                              long long ntiles, int grid_keygen, int mode, cudaStream_t st);
+// Segmented plan: keygen with per-(table, digit) counts, then 2 onesweep passes over row digits
+// of seg_db bits, tiles aligned to tables (ntiles_max = ceil(n / tile) + T; surplus CTAs exit).
+cudaError_t launch_sort_plan_seg(const SortParams& S, const PassParams* passes, int npasses,
+                                 long long ntiles_max, int grid_keygen, cudaStream_t st);
+size_t seg_sort_smem(int db, bool weights);
 cudaError_t plan_backward(const BwdParams& P, int threads, int share, unsigned* grid,
                           size_t* smem);
 cudaError_t launch_backward(const BwdParams& P, unsigned grid, int threads, size_t smem,

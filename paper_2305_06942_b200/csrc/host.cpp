@@ -148,6 +148,9 @@ struct emb_a2a {
   unsigned* d_hist = nullptr;            // 2 x ([kMaxPasses][256] digit counts + kMaxPasses tile
                                          // tickets) + the backward chunk ticket
   int hist_par = 0;                      // the half the next plan uses (keygen zeroes the other)
+  unsigned* d_shist = nullptr;           // segmented plan: 2 x ([2][T][NB] counts + 2 tickets)
+  size_t shist_half = 0;                 // words per half
+  int last_seg = -1;                     // mode of the previous plan (-1: none yet)
   unsigned* d_cnt = nullptr;             // radix pass: [256][ntiles] tile digit counts
   size_t cnt_cap = 0;
   unsigned long long* d_status = nullptr;  // onesweep look-back words
@@ -245,6 +248,10 @@ void release_registration(emb_a2a* h) {
   }
   h->plan_cap = h->wts_cap = 0;
   if (h->d_hist) cudaFree(h->d_hist);
+  if (h->d_shist) cudaFree(h->d_shist);
+  h->d_shist = nullptr;
+  h->shist_half = 0;
+  h->last_seg = -1;
   if (h->d_cnt) cudaFree(h->d_cnt);
   if (h->d_status) cudaFree(h->d_status);
   if (h->d_lbg) cudaFree(h->d_lbg);
@@ -1100,7 +1107,20 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   // DLRM-wide / sweep / weak, but the (row, table) order it leaves makes the reduction jump
   // between tables: pass 1 of DLRM-wide 401 -> 451 us, more than the plan saved.)
   const int kbits = tbits + rbits;
-  const int passes = (kbits + 7) / 8;
+  // Segmented plan (backward.cu "segmented sort plan"): the input is table-major and the sort
+  // stable, so sorting each table's segment by its row bits alone gives the same (table, row)
+  // order in 2 passes of <= 11-bit digits where the plain key needs 3 or 4.
+  int dev0 = 0, sms0 = 0;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  const int seg_db = std::max(8, (rbits + 1) / 2);
+  const int64_t ntiles_seg = (num_indices + kSortTile - 1) / kSortTile + h->T;
+  // Measured (r02o, ncu launch list): a 10-bit segmented pass costs 16.9 us and an 11-bit one
+  // 22.4 us against 12.0 us for an 8-bit pass (publishing and looking back over 4-8x the digit
+  // words), so 2 wide passes only tie 3-4 narrow ones; auto keeps the plain plan (option 3 only).
+  const bool seg = h->T >= 1 && h->T <= 256 && rbits <= 22 && h->sort_mode == 3;
+  (void)sms0;
+  const int passes = seg ? 2 : (kbits + 7) / 8;
   const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
@@ -1129,7 +1149,10 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     if ((rc = grow(h, &h->d_cnt, scap))) return rc;
     h->cnt_cap = scap;
   }
-  const size_t nstatus = (size_t)passes * ntiles * 256;   // onesweep look-back words
+  const size_t nb_seg = (size_t)1 << seg_db;
+  const long long ngroups_seg = (ntiles_seg + kSegLb - 1) / kSegLb + h->T;
+  const size_t nstatus = seg ? (size_t)2 * ntiles_seg * nb_seg
+                             : (size_t)passes * ntiles * 256;   // onesweep look-back words
   if (nstatus > h->status_cap) {
     const size_t scap = nstatus + nstatus / 4 + 4 * 256;
     if ((rc = grow(h, &h->d_status, scap))) return rc;
@@ -1137,7 +1160,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     h->status_cap = scap;
   }
   const long long ngroups = (ntiles + kLbGroup - 1) / kLbGroup;
-  const size_t nlbg = (size_t)passes * ngroups * 257;      // zeroed by keygen every plan
+  const size_t nlbg = seg ? (size_t)2 * ngroups_seg * (nb_seg + 1)
+                          : (size_t)passes * ngroups * 257;      // zeroed by keygen every plan
   if (nlbg > h->lbg_cap) {
     const size_t scap = nlbg + nlbg / 4 + 257;
     if ((rc = grow(h, &h->d_lbg, scap))) return rc;
@@ -1148,6 +1172,22 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     if ((rc = grow(h, &h->d_scratch, cap * 2 * h->D))) return rc;
     if ((rc = grow(h, &h->d_info, cap))) return rc;
     h->chunk_cap = cap;
+  }
+  if (seg) {
+    const size_t half = (size_t)2 * h->T * nb_seg + 2;
+    if (half > h->shist_half) {
+      if (h->d_shist) cudaFree(h->d_shist);
+      h->d_shist = nullptr;
+      h->shist_half = 0;
+      if ((rc = grow(h, &h->d_shist, 2 * half))) return rc;
+      CUDA_TRY(h, cudaMemsetAsync(h->d_shist, 0, 2 * half * 4, st));
+      h->shist_half = half;
+    }
+  }
+  if (n > 0 && h->last_seg >= 0 && h->last_seg != (seg ? 1 : 0)) {
+    // switching plan kinds breaks the "keygen zeroes the next plan's half" chain: clean both
+    CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, 2 * kHistWords * sizeof(unsigned), st));
+    if (h->d_shist) CUDA_TRY(h, cudaMemsetAsync(h->d_shist, 0, 2 * h->shist_half * 4, st));
   }
   h->plan_no += 1;
   h->rbits = rbits;
@@ -1209,13 +1249,41 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long TB = (long long)h->T * h->B;
   const long long gk = std::min<long long>((TB + 63) / 64, (long long)sms * 8);   // 8 bags/warp
-  cudaError_t e = launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1),
-                                   (int)h->sort_mode, st);
+  if (seg) {
+    unsigned* const sh = h->d_shist + (size_t)h->hist_par * h->shist_half;
+    S.seg_db = seg_db;
+    S.T = h->T;
+    S.shist = sh;
+    S.shist_clear = h->d_shist + (size_t)(1 - h->hist_par) * h->shist_half;
+    S.shist_words = (long long)h->shist_half;
+    const unsigned m0 = (1u << seg_db) - 1u;
+    const unsigned m1 = rbits > seg_db ? (1u << (rbits - seg_db)) - 1u : 0u;
+    for (int p = 0; p < 2; ++p) {
+      PassParams& q = pp[p];
+      q.status = h->d_status + (size_t)p * ntiles_seg * nb_seg;
+      q.tile_ctr = sh + (size_t)2 * h->T * nb_seg + p;
+      q.garrive = h->d_lbg + (size_t)p * ngroups_seg * (nb_seg + 1);
+      q.gsum = q.garrive + ngroups_seg;
+      q.ntiles = ntiles_seg;
+      q.shift = p * seg_db;
+      q.dmask = p == 0 ? m0 : m1;
+      q.offsets = offsets;
+      q.B = h->B;
+      q.T = h->T;
+      q.shist = sh + (size_t)p * h->T * nb_seg;
+    }
+  }
+  cudaError_t e = seg ? launch_sort_plan_seg(S, pp, passes, ntiles_seg,
+                                             (int)std::max<long long>(gk, 1), st)
+                      : launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1),
+                                         (int)h->sort_mode, st);
   if (e != cudaSuccess) {
     h->planned = false;
     cudaMemsetAsync(h->d_hist, 0, 2 * kHistWords * sizeof(unsigned), st);   // both halves clean
+    if (h->d_shist) cudaMemsetAsync(h->d_shist, 0, 2 * h->shist_half * 4, st);
     return fail(h, EMB_A2A_ECUDA, "backward plan launch: %s", cudaGetErrorString(e));
   }
+  if (n > 0) h->last_seg = seg ? 1 : 0;
   h->hist_par ^= 1;
   h->kernel_launches += 1 + passes;
   return EMB_A2A_OK;
@@ -1378,7 +1446,7 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "pdl_rows_early in {0, 1, 2}");
     h->rows_early = v;
   } else if (k == "sort_mode") {
-    if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2}");
+    if (v < 0 || v > 3) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3}");
     h->sort_mode = v;
   } else if (k == "bwd_threads") {
     // bwd_kernel is compiled with __launch_bounds__(128, ...): more threads cannot launch

@@ -497,3 +497,92 @@ def test_full_size_backward_sampled_rows(name):
         tol = 2 * (n * U / (1 - n * U)) * S + 4 * U * np.abs(want) + 1e-30
         assert np.all(np.abs(got.astype(np.float64) - want) <= tol), t
     h.destroy()
+
+
+def _seg_problem(seed, W, weighted=False, rows=(300, 4000)):
+    """Several sort tiles per table (look-back groups of 4 tiles), Zipf-like repeats, exact-int
+    values; rows drawn from `rows` (2^17..2^22 reaches every segmented digit width)."""
+    rng = np.random.default_rng(seed)
+    T = [int(rng.integers(1, 4)) for _ in range(W)]
+    D = 8
+    B = 1024 * W
+    G = sum(T)
+    R = [int(rng.integers(rows[0], rows[1])) for _ in range(G)]
+    tables = [rng.integers(-8, 8, size=(R[g], D)).astype(np.float32) for g in range(G)]
+    indices, offsets = [], []
+    g = 0
+    for r in range(W):
+        bags_t = []
+        for t in range(T[r]):
+            L = rng.integers(0, 24, size=B)
+            hot = rng.integers(0, R[g], size=16)          # repeated rows, runs across tiles
+            flat = np.where(rng.random(int(L.sum())) < 0.3, rng.choice(hot, size=int(L.sum())),
+                            rng.integers(0, R[g], size=int(L.sum())))
+            cuts = np.concatenate([[0], np.cumsum(L)])
+            bags_t.append([list(flat[cuts[b]:cuts[b + 1]]) for b in range(B)])
+            g += 1
+        i, o = csr_from_bags(bags_t)
+        indices.append(i)
+        offsets.append(o)
+    p = Problem(W, T, D, B, synth.even_partition(B, W), tables, indices, offsets)
+    w = [rng.integers(1, 4, size=i.size).astype(np.float32) for i in indices] if weighted else None
+    return p, w
+
+
+@pytest.mark.parametrize("seed,W,weighted", [(0, 1, False), (1, 1, True), (2, 2, False),
+                                             (3, 4, False)])
+def test_segmented_plan_exact_vs_oracle(seed, W, weighted):
+    """The segmented sort plan (sort_mode 3: each table's segment sorted by row bits only, 2
+    passes, tiles aligned to tables) gives the oracle's tables bitwise in exact-int mode."""
+    p, w = _seg_problem(7100 + seed, W, weighted)
+    grads = grads_for(p, seed, 1)
+    kw = {} if w is None else {"weights": w}
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 0.5, **kw)
+    run = Run(p, opts={"sort_mode": 3})
+    run.backward(grads, 0.5, weights=w)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+@pytest.mark.parametrize("seed,W,weighted,rows", [(0, 1, False, (1 << 16, 1 << 18)),
+                                                  (1, 1, True, (1 << 18, 1 << 20)),
+                                                  (2, 2, False, (1 << 20, 1 << 22)),
+                                                  (3, 1, False, (1 << 21, 1 << 22))])
+def test_segmented_plan_equals_plain_plan_wide_digits(seed, W, weighted, rows):
+    """17..22 row bits (digit widths 9, 10, 11): the segmented plan (sort_mode 3) produces the
+    plain (table, row) plan's order, so the updated tables are bitwise those of
+    sort_mode 1 (the plain plan is pinned to the oracle by the tests above)."""
+    p, w = _seg_problem(7150 + seed, W, weighted, rows)
+    grads = grads_for(p, seed, 1)
+    outs = []
+    for mode in (1, 3):
+        run = Run(p, opts={"sort_mode": mode})
+        run.backward(grads, 0.5, weights=w)
+        outs.append(run.tables())
+        run.destroy()
+    for got in outs[1:]:
+        for a, b in zip(got, outs[0]):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_segmented_plan_stall_reports_timeout():
+    """The segmented look-back's broken-invariant path (debug_sort_stall) reports ETIMEOUT."""
+    from paper_2305_06942_b200 import EmbA2AError
+    p, _ = _seg_problem(7200, 1)
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0), {"sort_mode": 3, "timeout_ms": 300})
+    tabs = [torch.from_numpy(t).to(dev()) for t in p.tables]
+    h.register_tables(tabs, p.B)
+    idx = torch.from_numpy(p.indices[0]).to(dev())
+    off = torch.from_numpy(p.offsets[0]).to(dev())
+    h.backward_plan(idx, off)
+    torch.cuda.synchronize()
+    h.check()
+    h.set_option("debug_sort_stall", 1)
+    h.backward_plan(idx, off)
+    torch.cuda.synchronize()
+    with pytest.raises(EmbA2AError) as e:
+        h.check()
+    assert "ETIMEOUT" in str(e.value)
+    h.destroy()
