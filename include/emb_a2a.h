@@ -248,6 +248,10 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *                  With peers, stores into a peer wait for that peer's credit (it has started
  *                  the same forward, so it consumed the buffer half they overwrite); off when a
  *                  peer shares this GPU (its CTAs could need the slots), 2 = on even then
+ *   "debug_credit_lag"  -1 (default): a peer's store into this rank's buffer half waits for this
+ *                  rank to have started the same forward (0) -- or, when a peer shares this GPU,
+ *                  the previous one (1, the weaker consumer contract); 0 / 1 force it (tests of
+ *                  the one-GPU-per-rank protocol on one GPU, with grids small enough to co-reside)
  *                  (tests, small grids)
  *   "vec"          float4s per lane per row, 1/2/4/8 (0 = auto): lanes per bag = D/(4*vec);
  *                  fewer lanes per bag keeps more bags in flight per warp

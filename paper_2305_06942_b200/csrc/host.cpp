@@ -85,6 +85,7 @@ struct emb_a2a {
   int64_t S = 32, order = 0, threads = 256, timeout_ms = 10000, validate = 0, unroll = 0;
   int64_t delay_ns = 0, skip_to = -1, idx_cap = 2048, stages = 4, ctas_per_sm = 0, tma = 0;
   int64_t stage_kb = 32, vec = 0, pdl = 1, flat_below = 12, rows_early = 1;
+  int64_t credit_lag_opt = -1;           // debug: -1 auto (1 iff a peer shares the GPU), 0, 1
   bool tables_dirty = true;              // a table writer may precede the next forward
   bool shared_gpu = false;               // some peer runs on this same GPU
   int64_t chunk = 32;
@@ -368,7 +369,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   // peer's kernel needs.  That keeps the weaker contract (a consumer ordered before our next
   // forward); one GPU per rank gives the full one (output valid until the second following
   // forward).
-  P.credit_lag = h->shared_gpu ? 1 : 0;
+  P.credit_lag = h->credit_lag_opt >= 0 ? (int)h->credit_lag_opt : (h->shared_gpu ? 1 : 0);
   P.flat_below = (int)h->flat_below;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
@@ -1445,6 +1446,9 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
   } else if (k == "pdl_rows_early") {
     if (v < 0 || v > 2) return fail(h, EMB_A2A_EINVAL, "pdl_rows_early in {0, 1, 2}");
     h->rows_early = v;
+  } else if (k == "debug_credit_lag") {
+    if (v < -1 || v > 1) return fail(h, EMB_A2A_EINVAL, "debug_credit_lag in {-1, 0, 1}");
+    h->credit_lag_opt = v;
   } else if (k == "sort_mode") {
     if (v < 0 || v > 3) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3}");
     h->sort_mode = v;
@@ -1489,6 +1493,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
   else if (k == "pdl_rows_early") *v = h->rows_early;
+  else if (k == "debug_credit_lag") *v = h->credit_lag_opt;
   else if (k == "sort_mode") *v = h->sort_mode;
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;

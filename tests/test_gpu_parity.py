@@ -376,6 +376,52 @@ def test_slow_consumer_rank_peers_run_ahead(W, early):
     g.destroy()
 
 
+@pytest.mark.parametrize("W", [2, 4])
+def test_dedicated_gpu_credit_protocol_late_consumer(W):
+    """The one-GPU-per-rank contract (credit lag 0: a peer stores into rank 0's half e&1, which
+    holds output e-2, only after rank 0 started forward e), forced on one GPU with early
+    programmatic launch (pdl_rows_early 2) and grids small enough to co-reside: rank 0 consumes
+    output e only AFTER issuing forward e+1 (allowed: valid until the second following forward),
+    slowly, while its peers run ahead; every copy equals the oracle."""
+    from paper_2305_06942_b200 import LoopbackGroup
+    cfg = synth.config_for("tiny", W=W, B=64)
+    probs = [from_config(cfg, k) for k in range(5)]
+    g = LoopbackGroup(W, dev(), {"slice": 4, "chunk": 16, "pdl_rows_early": 2,
+                                 "debug_credit_lag": 0, "timeout_ms": 8000, "ctas_per_sm": 1})
+    tabs = [[torch.from_numpy(t).to(dev()) for t in probs[0].rank_tables(r)] for r in range(W)]
+    g.register_tables(tabs, cfg.B, cfg.part)
+    csr = [dev_csr(pr) for pr in probs]
+    torch.cuda._sleep(10)
+    torch.zeros(4, device=dev()).clone()
+    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream()
+    for s_ in g.streams:
+        s_.wait_stream(cur)
+    outs = {r: [] for r in range(W)}
+    copies = []
+    for e in range(5):
+        for r, h in enumerate(g.handles):
+            st = g.streams[r]
+            outs[r].append(h.forward(csr[e][0][r], csr[e][1][r], stream=st))
+            if r == 0 and e >= 1:     # consume output e-1 after issuing forward e
+                with torch.cuda.stream(st):
+                    torch.cuda._sleep(20_000_000)
+                    copies.append(outs[0][e - 1].clone())
+    with torch.cuda.stream(g.streams[0]):
+        copies.append(outs[0][4].clone())
+    for s_ in g.streams:
+        cur.wait_stream(s_)
+    torch.cuda.synchronize()
+    for h in g.handles:
+        h.check()
+    for e in range(5):
+        np.testing.assert_array_equal(copies[e].cpu().numpy(), oracle_out(probs[e])[0])
+    ref = oracle_out(probs[4])
+    for r in range(1, W):
+        np.testing.assert_array_equal(outs[r][4].cpu().numpy(), ref[r])
+    g.destroy()
+
+
 def test_forward_host_back_to_back_double_buffered_staging():
     """Six forward_host calls without a sync in between (inputs of different sizes, so the
     staging regrows once; the two staging buffers alternate and each call's input copy runs on
