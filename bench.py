@@ -657,6 +657,7 @@ def main():
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
                    "order": h.get_option("order"), "ctas_per_sm": h.get_option("ctas_per_sm"),
+                   "chunk_bags": h.query("chunk_bags"),
                    "skew_us_last_rank": args.skew_us,
                    "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
                           "distinct rows) over %.1f GB of tables, K back-to-back steps" %

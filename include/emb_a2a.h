@@ -226,9 +226,11 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *   "out_dtype"    output element type (emb_a2a_dtype): 0 fp32 (default), 1 bf16, 2 fp16 --
  *                  accumulation stays fp32, the result is rounded once (R#32); identical on all
  *                  ranks, set before register_tables (the receive buffers are sized for it)
- *   "chunk"        bags per work ticket, 1..63 (default 32; the largest divisor of S not above
- *                  it is used): load-balance granularity, independent of the signal slice S
- *                  (set before register_tables)
+ *   "chunk"        bags per work ticket, 1..127, or 0 (default): per forward, about 640
+ *                  lookups per ticket from the forward's average bag length, 32..127 bags.
+ *                  Load-balance granularity, rank-local, independent of the signal slice S --
+ *                  a chunk's bags count toward every slice they fall in (set before
+ *                  register_tables)
  *   "threads"      consumer threads per CTA, multiple of 32 in [32, 256] (default 256); each
  *                  CTA also has one producer warp
  *   "timeout_ms"   receive-wait timeout (default 10000)

@@ -436,7 +436,8 @@ struct StageHdr {
   int staged;         // payload holds this stage's rows / indices
   int flat;           // short bags: row-flattened pooling (average length < flat_below)
   int remote;         // fused, s != r: count the stage's bags toward its slice when consumed
-  int slice_id, slice_bags;
+  int slice_id, slice_bags;   // the slice holding row0 and its bag count
+  int bs;             // destination block size b_s (a stage may run on into later slices)
   long long j0;       // global sample of the first bag
   char* out_base;     // fused: recv_s[parity]; pool: send (elements of the output type)
   unsigned long long* flag;
@@ -571,17 +572,27 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
           // every consumer store of this stage happens-before this point (mbarrier
           // release/acquire); make them visible system-wide before counting them (R#25)
           fence_acq_rel_sys();
-          const unsigned long long old =
-              atom_add_acqrel_gpu(P.slice_cnt + h->slice_id, (unsigned long long)h->nb);
-          if (old + (unsigned long long)h->nb ==
-                  P.epoch * (unsigned long long)h->slice_bags &&
-              h->s != P.skip_to) {
-            if (P.delay_ns > 0) {
-              const unsigned long long t0 = globaltimer();
-              while (globaltimer() - t0 < (unsigned long long)P.delay_ns) __nanosleep(1000);
+          // the stage's bags [row0, row0 + nb) count toward each slice they fall in (a chunk
+          // may be longer than a slice: chunks are work units, slices signal units)
+          int row = h->row0, left = h->nb, sid = h->slice_id, sbags = h->slice_bags;
+          while (left > 0) {
+            const int in_slice = P.S - row % P.S;
+            const int take = left < in_slice ? left : in_slice;
+            const unsigned long long old =
+                atom_add_acqrel_gpu(P.slice_cnt + sid, (unsigned long long)take);
+            if (old + (unsigned long long)take == P.epoch * (unsigned long long)sbags &&
+                h->s != P.skip_to) {
+              if (P.delay_ns > 0) {
+                const unsigned long long t0 = globaltimer();
+                while (globaltimer() - t0 < (unsigned long long)P.delay_ns) __nanosleep(1000);
+              }
+              red_release_sys_add(h->flag, 1ull);   // P:151 PUT -> fence -> sliceRdy
+              ++signalled;
             }
-            red_release_sys_add(h->flag, 1ull);   // P:151 PUT -> fence -> sliceRdy
-            signalled = 1;
+            row += take;
+            left -= take;
+            ++sid;
+            sbags = (h->bs - row) < P.S ? h->bs - row : P.S;
           }
         }
       }
@@ -610,23 +621,26 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
     };
     int ticket = (int)blockIdx.x;
     int k, s, t, i0, nb;
-    int o0 = 0, o1 = 0;   // chunk offsets: lane q holds off[q] and off[32 + q]
+    // chunk offsets (C <= 127 bags): lane q holds off[q], off[32 + q], off[64 + q], off[96 + q]
+    int o0 = 0, o1 = 0, o2 = 0, o3 = 0;
     auto load_offsets = [&](int tk, int& kk, int& ss, int& tt, int& ii, int& nn, int& a,
-                            int& b2) {
+                            int& b2, int& c2, int& d2) {
       decode_unit(P, tk, P.C, P.chunk_base, kk, ss, tt, ii, nn);
       const int* offg = P.offsets + (long long)tt * P.B + P.part[ss] + ii;
       if (lane32 <= nn) a = __ldg(offg + lane32);
       if (32 + lane32 <= nn) b2 = __ldg(offg + 32 + lane32);
+      if (64 + lane32 <= nn) c2 = __ldg(offg + 64 + lane32);
+      if (96 + lane32 <= nn) d2 = __ldg(offg + 96 + lane32);
     };
-    auto off_at = [&](int e) { return warp_bcast(e < 32 ? o0 : o1, e & 31); };
-    if (ticket < P.nchunks) load_offsets(ticket, k, s, t, i0, nb, o0, o1);
+    auto off_at = [&](int e) {
+      return warp_bcast(e < 64 ? (e < 32 ? o0 : o1) : (e < 96 ? o2 : o3), e & 31);
+    };
+    if (ticket < P.nchunks) load_offsets(ticket, k, s, t, i0, nb, o0, o1, o2, o3);
     while (ticket < P.nchunks) {
       const int tk_next = ticket + (int)gridDim.x;
-      int k2 = 0, s2 = 0, t2 = 0, i02 = 0, nb2 = 0, p0 = 0, p1 = 0;
-      if (tk_next < P.nchunks) load_offsets(tk_next, k2, s2, t2, i02, nb2, p0, p1);
+      int k2 = 0, s2 = 0, t2 = 0, i02 = 0, nb2 = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+      if (tk_next < P.nchunks) load_offsets(tk_next, k2, s2, t2, i02, nb2, p0, p1, p2, p3);
       if (lane32 == 0) trace_ev(P, 1, (unsigned)ticket);
-      int slice_id = 0, slice_bags = 0;
-      if (FUSED) slice_of_chunk(P, k, s, t, i0, slice_id, slice_bags);
       const long long j0 = P.part[s] + i0;
       for (int cb = 0; cb < nb;) {    // usually one stage per chunk
         const int st = u % NS;
@@ -647,6 +661,10 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
         // stage-local offsets
         if (lane32 >= cb && lane32 <= cb + n) so[lane32 - cb] = o0;
         if (32 + lane32 >= cb && 32 + lane32 <= cb + n) so[32 + lane32 - cb] = o1;
+        if (64 + lane32 >= cb && 64 + lane32 <= cb + n) so[64 + lane32 - cb] = o2;
+        if (96 + lane32 >= cb && 96 + lane32 <= cb + n) so[96 + lane32 - cb] = o3;
+        int slice_id = 0, slice_bags = 0;
+        if (FUSED) slice_of_chunk(P, k, s, t, i0 + cb, slice_id, slice_bags);
         if (lane32 == 0) {
           StageHdr* h = hdr(st);
           h->end = 0; h->s = s; h->t = t; h->row0 = i0 + cb; h->nb = n; h->base = base;
@@ -655,6 +673,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
           h->remote = (FUSED && s != P.r) ? 1 : 0;
           h->slice_id = slice_id;
           h->slice_bags = slice_bags;
+          h->bs = (int)(P.part[s + 1] - P.part[s]);
           h->out_base = s_out[s];
           h->flag = s_flag[s];
         }
@@ -701,7 +720,7 @@ __global__ void __launch_bounds__(288, TMA ? 1 : EMBA2A_LSU_MINB(NV))
         ++u;
       }
       ticket = tk_next;
-      k = k2; s = s2; t = t2; i0 = i02; nb = nb2; o0 = p0; o1 = p1;
+      k = k2; s = s2; t = t2; i0 = i02; nb = nb2; o0 = p0; o1 = p1; o2 = p2; o3 = p3;
     }
     // end marker, then drain: every outstanding stage is consumed and published
     pdl_wait_once();

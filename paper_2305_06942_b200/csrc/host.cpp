@@ -88,7 +88,7 @@ struct emb_a2a {
   int64_t credit_lag_opt = -1;           // debug: -1 auto (1 iff a peer shares the GPU), 0, 1
   bool tables_dirty = true;              // a table writer may precede the next forward
   bool shared_gpu = false;               // some peer runs on this same GPU
-  int64_t chunk = 32;
+  int64_t chunk = 0;                     // 0 = auto per forward (auto_chunk)
   int64_t trace_cap = 0;                 // records; 0 = tracing off
   unsigned long long* d_trace = nullptr;
 
@@ -289,17 +289,28 @@ int barrier(emb_a2a* h) {
   return EMB_A2A_OK;
 }
 
-// Chunk size: the largest divisor of S that is <= the "chunk" option (and <= 63, the producer
-// keeps a chunk's offsets in two registers per lane).
+// Chunk size (bags per work unit): the "chunk" option, at most 127 (the producer keeps a chunk's
+// offsets in four registers per lane).  Chunks and slices are independent: a stage's bags count
+// toward every slice they fall in (fused_kernel.cuh recycle).
 int chunk_size(int64_t S, int64_t want) {
-  int64_t c = std::min<int64_t>(std::min<int64_t>(want, S), 63);
-  while (c > 1 && S % c != 0) --c;
-  return (int)std::max<int64_t>(c, 1);
+  (void)S;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, 127));
+}
+
+// Chunk size when the "chunk" option is 0 (default): about 640 lookups per work unit from this
+// forward's average bag length, 32..127 bags.  Measured (r02u, one B200, per-rank work at W=1):
+// short bags need long chunks (sweep P=1: 31.5 us at 32 bags -> 23.2 us at 127; P=4 44.1 ->
+// 41.7), long bags short ones (DLRM-small 12.9 us at 32 vs 14.3 at 64; weak 19.4 vs 23.0;
+// DLRM-wide 193 vs 203).  Chunks are rank-local work units: no peer needs to agree.
+int auto_chunk(const emb_a2a* h, int64_t nnz) {
+  const int64_t bags = (int64_t)h->T * h->B;
+  if (bags <= 0 || nnz <= 0) return 127;
+  return (int)std::max<int64_t>(32, std::min<int64_t>(127, (640 * bags) / nnz));
 }
 
 // Slice and chunk counts per destination ordinal (row a1): T * ceil(b_s / unit).
-void compute_slices(emb_a2a* h) {
-  h->C = chunk_size(h->S, h->chunk);
+void compute_slices(emb_a2a* h, int C) {
+  h->C = C;
   int64_t acc = 0, accc = 0;
   for (int k = 0; k < h->W; ++k) {
     h->slice_base[k] = (int)acc;
@@ -316,6 +327,18 @@ void compute_slices(emb_a2a* h) {
   for (int q = 0; q < h->W; ++q) {
     const int64_t nsl = (h->b + h->S - 1) / h->S;
     h->host_peers.n_in[q] = (q == h->rank) ? 0 : (long long)h->allT[q] * nsl;
+  }
+}
+
+// Re-derive the chunk plan when this forward's chunk size differs from the last one (the
+// cached launch configurations depend on it: grid = min(slots, chunks), stage layout).
+void ensure_chunk(emb_a2a* h, int64_t nnz) {
+  const int C = h->chunk > 0 ? chunk_size(h->S, h->chunk) : auto_chunk(h, nnz);
+  if (C == h->C) return;
+  compute_slices(h, C);
+  for (int w = 0; w < 2; ++w) {
+    h->plan_fused[w] = LaunchPlan();
+    h->plan_pool[w] = LaunchPlan();
   }
 }
 
@@ -702,7 +725,7 @@ static int register_impl(emb_a2a_t* h, int num_local_tables, const void* const* 
     CUDA_TRY(h, cudaMemcpy(h->d_rows, r64.data(), sizeof(long long) * h->T,
                            cudaMemcpyHostToDevice));
   }
-  compute_slices(h);
+  compute_slices(h, h->chunk > 0 ? chunk_size(h->S, h->chunk) : 32);
   {
     const int rc_maps = make_tensor_maps(h, tables);
     if (rc_maps) return rc_maps;
@@ -759,6 +782,7 @@ int emb_a2a_forward_weighted(emb_a2a_t* h, const int32_t* indices, const int32_t
     return fail(h, EMB_A2A_EINVAL, "weights must be 4-byte aligned");
   h->epoch += 1;
   const float* w = num_indices > 0 ? weights : nullptr;
+  ensure_chunk(h, num_indices);
   KParams P = make_params(h, indices, offsets, w);
   // consumers may gather rows and store before the predecessor completes when no backward of
   // this handle (the only table writer) ran since the previous forward; with peers, the
@@ -962,6 +986,7 @@ int emb_a2a_pool_local_weighted(emb_a2a_t* h, const int32_t* indices, const int3
   if (weights && h->mean)
     return fail(h, EMB_A2A_EINVAL, "per-sample weights need sum pooling (R#26)");
   const float* w = num_indices > 0 ? weights : nullptr;
+  ensure_chunk(h, num_indices);
   KParams P = make_params(h, indices, offsets, w);
   P.send = send;
   P.done = h->d_done + 2;      // own counters: may run concurrently with a forward's kernel
@@ -1396,7 +1421,7 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
       return fail(h, EMB_A2A_ESTATE, "set 'out_dtype' before register_tables");
     h->out_dtype = v;
   } else if (k == "chunk") {
-    if (v < 1 || v > 63) return fail(h, EMB_A2A_EINVAL, "chunk in [1, 63]");
+    if (v < 0 || v > 127) return fail(h, EMB_A2A_EINVAL, "chunk in [0 (auto), 127]");
     if (h->registered && v != h->chunk)
       return fail(h, EMB_A2A_ESTATE, "set 'chunk' before register_tables");
     h->chunk = v;

@@ -229,19 +229,23 @@ def test_forward_host_batch_multi_rank_loopback():
 
 # ------------------------------------------------------------------ trace (E1) and counts
 
-@pytest.mark.parametrize("W,S", [(2, 4), (4, 7)])
-def test_trace_invariance_and_signal_counts(W, S):
+@pytest.mark.parametrize("W,S,C", [(2, 4, 0), (4, 7, 0), (2, 4, 16), (4, 7, 20)])
+def test_trace_invariance_and_signal_counts(W, S, C):
     """The trace option (P:239-258 per-WG timeline) changes no result: outputs with trace on
     equal the trace-off outputs and the oracle bitwise.  Each rank's trace logs exactly one
-    'signalled' release (event 3, payload 1) per remote slice: sum over s != r of
-    T_r * ceil(b_s / S), which is also what the destinations' counters grew by."""
+    release per remote slice (event 3, payload = slices released by that stage; a chunk C
+    longer than a slice S releases several): sum over s != r of T_r * ceil(b_s / S),
+    which is also what the destinations' counters grew by."""
     from paper_2305_06942_b200 import LoopbackGroup
     cfg = synth.config_for("tiny", W=W, B=64 if W == 2 else 96)
     p = from_config(cfg, 0)
     ref = oracle_out(p)
     outs = {}
     for trace in (0, 1 << 16):
-        g = LoopbackGroup(W, dev(), {"slice": S, "trace": trace})
+        opts = {"slice": S, "trace": trace}
+        if C:
+            opts["chunk"] = C
+        g = LoopbackGroup(W, dev(), opts)
         tabs = [[torch.from_numpy(t).to(dev()) for t in p.rank_tables(r)] for r in range(W)]
         g.register_tables(tabs, cfg.B)
         idx = [torch.from_numpy(i).to(dev()) for i in p.indices]
@@ -254,7 +258,7 @@ def test_trace_invariance_and_signal_counts(W, S):
             for r, h in enumerate(g.handles):
                 tr = h.read_trace()
                 assert tr.size < (1 << 16)
-                sent = int(((tr["event"] == 3) & (tr["payload"] == 1)).sum())
+                sent = int(tr["payload"][tr["event"] == 3].sum())
                 want = sum(oracle.signal_count(r, s, cfg.T, cfg.part, S) for s in range(W) if s != r)
                 assert sent == nfwd * want, (r, sent, want)
                 # one receive-wait-done record per forward (the last CTA), for W > 1
