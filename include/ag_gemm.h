@@ -55,8 +55,9 @@ int ag_gemm_init(int rank, int world_size, int cuda_device, ag_gemm_allgather_fn
 
 /* Register the problem shape (collective; identical on all ranks, EINVAL otherwise).
  *  M        rows of X_r (tokens on this rank), M % 128 == 0, M >= 128.
- *  n_local  N_r rows of each rank's weight shard, N_r % 128 == 0; the GEMM N-tile is 256 when
- *           N_r % 256 == 0, else 128.  N = W * N_r < 2^31 / K.
+ *  n_local  N_r rows of each rank's weight shard, N_r % 128 == 0; the GEMM N-tile (= the
+ *           communication chunk) is 256 rows when N_r % 256 == 0, else 128 (option "bn").
+ *           N = W * N_r < 2^31 / K.
  *  K        reduction length, K % 64 == 0, K >= 64.
  *  out_f32  0: Y is bfloat16 (fp32 accumulator rounded once to nearest even); 1: Y is float32.
  * Allocates the symmetric region -- [ready flags W x chunks u32 | credits W x 128 B | gather
@@ -92,7 +93,9 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
  *                 remote tile times out) -- default 1
  *   "pair"        1: a cluster of two CTAs (one TPC) per 256 x BN tile, tcgen05.mma.cta_group::2,
  *                 each CTA staging its 128 A rows and half of the B rows (default; used when
- *                 M % 256 == 0); 0: one CTA per 128 x BN tile (cta_group::1) */
+ *                 M % 256 == 0); 0: one CTA per 128 x BN tile (cta_group::1)
+ *   "bn"          0 (default: 256 when N_r allows), 128 or 256: the N-tile (set before
+ *                 register) */
 int ag_gemm_set_option(ag_gemm_t* h, const char* key, int64_t value);
 int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* value);
 

@@ -14,7 +14,10 @@ Wr = torch.empty((cfg.N_r, cfg.K), dtype=torch.bfloat16, device=dev)
 fill_gemm_bf16(X, G.X_TENSOR, G.GEMM_SEED, 0); fill_gemm_bf16(Wr, G.W_TENSOR, G.GEMM_SEED, 0)
 Y = torch.empty((cfg.M, cfg.N), dtype=torch.bfloat16, device=dev)
 h = AgGemm(0, 1, dev, LocalGroup(1).allgather_for(0))
+if len(sys.argv) > 3:
+    h.set_option("bn", int(sys.argv[3]))
 h.register(cfg.M, cfg.N_r, cfg.K)
+print(json.dumps({"bn": h.query("bn"), "pair": h.query("pair")}))
 def t(steps=10):
     for _ in range(3): h.forward(X, Wr, Y)
     torch.cuda.synchronize()
@@ -35,9 +38,7 @@ if mode == "grid":
 elif mode == "ab":
     # interleaved A/B: every config measured once per round, 5 rounds; min and median reported
     import statistics
-    confs = [dict(pair=1, stages=6, group_m=16), dict(pair=1, stages=7, group_m=16),
-             dict(pair=1, stages=6, group_m=8), dict(pair=1, stages=6, group_m=32),
-             dict(pair=0, stages=6, group_m=16), "cublas"]
+    confs = [dict(pair=1, stages=6, group_m=16), dict(pair=0, stages=6, group_m=16), "cublas"]
     Yb = torch.empty_like(Y)
     res = {i: [] for i in range(len(confs))}
     for rnd in range(5):
