@@ -72,9 +72,9 @@ def parse():
     ap.add_argument("--ag-config", default="ag_ffn", help="ag_gemm workload (synth/gemm_gen.py)")
     ap.add_argument("--ag-order", type=int, default=-1, help="ag_gemm tile order (0 comm-aware, 1 ascending)")
     ap.add_argument("--ag-grid", type=int, default=0, help="ag_gemm persistent CTAs (0 = auto)")
-    ap.add_argument("--ag-leg", type=int, default=-1,
+    ap.add_argument("--ag-leg", type=int, default=1,
                     help="add the f4 AllGather+GEMM measurement to the main line as 'ag_gemm' "
-                         "(-1 = only at N=1, 0 = never, 1 = at every N)")
+                         "(1 = at every N, default; -1 = only at N=1; 0 = never)")
     return ap.parse_args()
 
 
@@ -633,7 +633,8 @@ def main():
             agl = bench_ag_gemm.measure(args, ROOT, dev, rank, N, shared, ClockSampler, host_cpu,
                                         "ag_tiny" if shared else args.ag_config,
                                         min(args.steps, 10), 3, with_e2e=False, with_cpu=False)
-            ag = {"metric": agl["metric"], "value": agl["value"], "unit": agl["unit"],
+            ag = agl if "error" in agl else {
+                  "metric": agl["metric"], "value": agl["value"], "unit": agl["unit"],
                   "ms_per_step": agl["ms_per_step"], "workload": agl["config"]["workload"],
                   "roofline": agl["roofline"], "unfused": agl["unfused"],
                   "parity_all_ranks": agl["parity_all_ranks"], "clocks": agl["clocks"],

@@ -103,6 +103,13 @@ def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, 
     Y = torch.empty((cfg.M, cfg.N), dtype=torch.bfloat16, device=dev)
     torch.cuda.synchronize()
 
+    def agree(ok):
+        """Every rank's verdict on the phase just run (MIN over ranks): a failure on one rank
+        stops all of them at the same point instead of leaving the others in a collective."""
+        t = torch.tensor([1 if ok else 0], device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
     h = AgGemm(rank, N, dev, torch_allgather(None, dev), {"timeout_ms": 60000} if shared else None)
     if getattr(args, "ag_order", -1) >= 0:
         h.set_option("order", args.ag_order)
@@ -110,6 +117,14 @@ def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, 
         h.set_option("grid", args.ag_grid)
     h.register(cfg.M, cfg.N_r, cfg.K)
     stream = torch.cuda.current_stream(dev)
+    failed = {}
+
+    def bail(where, err):
+        failed["where"] = where
+        failed["error"] = err
+        h.destroy()                  # collective; every rank reaches it at the same phase
+        return {"metric": METRIC_AG, "error": f"{where}: {err}"[:400], "n_gpus": N,
+                "config": {"workload": workload_desc(cfg)}, "parity_all_ranks": False}
 
     def max_over_ranks(x):
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
@@ -136,13 +151,20 @@ def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, 
         h.forward(X, Wr, Y, stream)
 
     clk = ClockSampler(local)
-    for _ in range(warmup):
-        fused()
-    torch.cuda.synchronize()
+    err = ""
+    try:
+        for _ in range(warmup):
+            fused()
+        torch.cuda.synchronize()
+    except Exception as e:          # host-side failure on this rank
+        err = repr(e)
+    if not agree(not err and h.status() == 0):
+        return bail("warm-up", err or f"device status {h.status()} (rank {rank})")
     clk.start()
     ms = b2b(fused, steps, 0)
     clocks = clk.stop()
-    h.check()
+    if not agree(h.status() == 0):
+        return bail("timed forwards", f"device status {h.status()} (rank {rank})")
     ms_step = max_over_ranks(ms) / steps
     flops = cfg.flops_per_rank()
     value = N * flops / (ms_step * 1e-3) / 1e12
@@ -152,7 +174,8 @@ def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, 
     # ---- parity: a fresh forward, sampled entries against one-at-a-time oracle dot products
     Yp, Wg = h.forward(X, Wr, None, stream)
     torch.cuda.synchronize()
-    h.check()
+    if not agree(h.status() == 0):
+        return bail("parity forward", f"device status {h.status()} (rank {rank})")
     rng = np.random.default_rng(1000 + rank)
     m = rng.integers(0, cfg.M, 128)
     n = rng.integers(0, cfg.N, 128)
@@ -280,6 +303,8 @@ def main(args, root, helpers):
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     line = measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, args.ag_config,
                    args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)
+    line.setdefault("value", 0.0)
+    line.setdefault("unit", "TFLOP/s")
     if shared:
         line["test_mode"] = "EMBA2A_SHARED_GPU=1: all ranks on one GPU; not a bench value"
     if rank == 0:

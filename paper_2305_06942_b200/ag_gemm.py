@@ -109,6 +109,10 @@ class AgGemm:
     def check(self) -> None:
         self._err(lib.ag_gemm_check(self._h), "ag_gemm_check")
 
+    def status(self) -> int:
+        """The asynchronous error status without raising (0 = OK)."""
+        return int(lib.ag_gemm_check(self._h))
+
     def destroy(self) -> None:
         if self._h:
             lib.ag_gemm_destroy(self._h)

@@ -47,6 +47,9 @@ def test_bench_torchrun_shared_gpu(n):
     assert roof["compulsory_bytes_per_launch"] <= roof["algorithmic_bytes_per_launch"]
     assert 0 < roof["frac_compulsory"] <= roof["frac"]
     assert line["alpha0"]["us_per_step"] > 0
+    ag = line["ag_gemm"]            # f4 leg at N ranks: fused AllGather + GEMM, parity on every rank
+    assert "error" not in ag, ag
+    assert ag["parity_all_ranks"] is True and ag["value"] > 0 and ag["roofline"]["bound"] == "tensor"
 
 
 @pytest.mark.gpu
