@@ -29,6 +29,16 @@ def tensor_peaks(root):
     return 2250.0, 2250.0, "fallback (nominal dense bf16 2.25 PFLOP/s)"
 
 
+def ncu_traffic(root, cfg):
+    """DRAM bytes per launch of ag_gemm_kernel for this workload from the committed ncu capture
+    (tools/ncu_traffic.sh -> profiles/ncu_traffic.json), or None."""
+    p = os.path.join(root, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    v = json.load(open(p)).get(f"{cfg.name}_W{cfg.W}")
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else None
+
+
 def workload_desc(cfg):
     return (f"{cfg.name} at W={cfg.W}: X_r [{cfg.M}][{cfg.K}] x AllGather(W_s [{cfg.N_r}][{cfg.K}], "
             f"s<{cfg.W}) -> Y_r [{cfg.M}][{cfg.N}], bf16 in / fp32 accumulate / bf16 out")
@@ -257,7 +267,10 @@ def measure(args, root, dev, rank, N, shared, ClockSampler, host_cpu, cfg_name, 
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "peak_source": peak_src, "frac": achieved / peak,
                      "frac_vs_sustained": achieved / peak_sus,
-                     "flops_per_launch": flops, "traffic": None},
+                     "flops_per_launch": flops, "traffic": ncu_traffic(root, cfg),
+                     "compulsory_bytes": 2 * (cfg.M * cfg.K + cfg.N * cfg.K + cfg.M * cfg.N),
+                     "traffic_note": "dram__bytes_read + write per launch from the committed ncu "
+                                     "capture (profiles/ncu_traffic.json), cold and serialised"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "unfused": {"ms_per_step": ms_b, "what": ("NCCL all_gather_into_tensor + torch.matmul "

@@ -4,7 +4,7 @@
 tag=${1:-r02}
 out=gpurun_out/matrix_$tag.jsonl
 mkdir -p gpurun_out
-run() { timeout 900 python bench.py --no-cpu --steps 30 --alpha0-batches 2 "$@" 2>>gpurun_out/matrix_$tag.err | tail -1 >> $out; echo "done: $*"; }
+run() { timeout 900 python bench.py --no-cpu --ag-leg 0 --steps 30 --alpha0-batches 2 "$@" 2>>gpurun_out/matrix_$tag.err | tail -1 >> $out; echo "done: $*"; }
 run --config dlrm_small
 run --config dlrm_small --table-dtype bf16
 run --config dlrm_small --table-dtype f16

@@ -10,9 +10,16 @@ for c in dlrm_small weak sweep_p1 sweep_p4 sweep_p8 sweep_p32 sweep_p128 dlrm_wi
   nb=4; [ $c = sweep_p128 ] && nb=2
   timeout 900 ncu --metrics $M --clock-control none -k regex:emb_a2a_kernel -s 3 -c 1 --csv \
     --log-file $O/$c.csv python bench.py --config $c --steps 3 --warmup 3 --batches $nb --no-cpu \
-    --no-baseline --no-backward --no-alpha0 > $O/$c.log 2>&1
+    --no-baseline --no-backward --no-alpha0 --ag-leg 0 > $O/$c.log 2>&1
   timeout 900 ncu --metrics $M --clock-control none -k regex:bwd_kernel -s 3 -c 1 --csv \
     --log-file $O/${c}_backward.csv python bench.py --config $c --steps 3 --warmup 3 --batches $nb \
-    --no-cpu --no-baseline --no-alpha0 > $O/${c}_backward.log 2>&1
+    --no-cpu --no-baseline --no-alpha0 --ag-leg 0 > $O/${c}_backward.log 2>&1
+  echo "done $c"
+done
+# f4: the fused AllGather + GEMM kernel (W = 1)
+for c in ag_ffn ag_small; do
+  timeout 900 ncu --metrics $M --clock-control none -k regex:ag_gemm_kernel -s 3 -c 1 --csv \
+    --log-file $O/$c.csv python bench.py --path ag_gemm --ag-config $c --steps 3 --warmup 2 \
+    --no-cpu > $O/$c.log 2>&1
   echo "done $c"
 done
