@@ -95,7 +95,10 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
  *                 each CTA staging its 128 A rows and half of the B rows (default; used when
  *                 M % 256 == 0); 0: one CTA per 128 x BN tile (cta_group::1)
  *   "bn"          0 (default: 256 when N_r allows), 128 or 256: the N-tile (set before
- *                 register) */
+ *                 register)
+ *   "l2hints"     L2 cache-policy bits (default 0 = none): 1 TMA loads of A evict_last, 2 of B
+ *                 evict_first, 4 Y written with streaming stores (st.global.cs) -- measured
+ *                 neutral to worse */
 int ag_gemm_set_option(ag_gemm_t* h, const char* key, int64_t value);
 int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* value);
 

@@ -66,6 +66,7 @@ struct Params {
   const unsigned long long* credit_in;  // own credits, slot q at q * 16
   unsigned* piece_ctr;                  // [W][chunks] monotone, local
   int chunks, pieces, comm, local_copy;
+  int l2hints;                          // bits: 1 A evict_last, 2 B evict_first, 4 Y streaming stores
   long long piece_u4;
   int* err;
   long long timeout_ns;
@@ -112,11 +113,32 @@ __device__ __forceinline__ bool mbar_wait(unsigned bar, unsigned parity, const P
   return true;
 }
 __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, unsigned bar,
-                                            int c0, int c1) {
+                                            int c0, int c1, unsigned long long policy) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(policy) : "memory");
+}
+// L2 policies: the A panel of an M-tile group is re-read for every N-tile of the group (keep
+// it), a B tile only by the group's consecutive M-tiles and Y is written once (let them go)
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_normal() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_stream_v4(void* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -239,11 +261,12 @@ __device__ __forceinline__ void cluster_sync_all() {
 // TMA load into this CTA's shared memory whose completion (bytes) is counted on the pair
 // leader's mbarrier (cta_group::2: the leader's MMA reads both CTAs' stages)
 __device__ __forceinline__ void tma_load_2d_pair(unsigned dst, const CUtensorMap* map,
-                                                 unsigned leader_bar, int c0, int c1) {
+                                                 unsigned leader_bar, int c0, int c1,
+                                                 unsigned long long policy) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(leader_bar) : "memory");
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy) : "memory");
 }
 
 // ------------------------------------------------------------------------------ tile order
@@ -350,6 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
       int ready_s = -1, ready_n = -1;
       bool ok = true;
       const unsigned lbar0 = PAIR ? mapa(full_bar(0), 0) : full_bar(0);   // leader's full[0]
+      const unsigned long long pol_a = (P.l2hints & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const unsigned long long pol_b = (P.l2hints & 2) ? l2_policy_evict_first() : l2_policy_evict_normal();
       for (int t = unit; t < ntiles && ok; t += nunits) {
         const Tile x = tile_of(P, t);
         const CUtensorMap* mb = &P.tmB_local;
@@ -388,12 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
             // barrier, multicast commit).  (A remote arrive per stage was a MEMBAR.GPU each.)
             const unsigned lb = lbar0 + 8u * stage;
             if (leader) mbar_expect_tx(full_bar(stage), 2 * (C::kABytes + C::kBBytes));
-            tma_load_2d_pair(da, &P.tmA, lb, kb * BK, arow);
-            tma_load_2d_pair(db, mb, lb, kb * BK, brow);
+            tma_load_2d_pair(da, &P.tmA, lb, kb * BK, arow, pol_a);
+            tma_load_2d_pair(db, mb, lb, kb * BK, brow, pol_b);
           } else {
             mbar_expect_tx(full_bar(stage), C::kABytes + C::kBBytes);
-            tma_load_2d(da, &P.tmA, full_bar(stage), kb * BK, arow);
-            tma_load_2d(db, mb, full_bar(stage), kb * BK, brow);
+            tma_load_2d(da, &P.tmA, full_bar(stage), kb * BK, arow, pol_a);
+            tma_load_2d(db, mb, full_bar(stage), kb * BK, brow, pol_b);
           }
           if (++stage == NS) { stage = 0; phase ^= 1u; }
         }
@@ -431,6 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     // ============================== epilogue ==================================
     const int q = warp & 3;                   // TMEM lanes 32q..32q+31 = tile rows
+    auto st_y = [&](uint4* p, const uint4& v) {
+      if (P.l2hints & 4) st_stream_v4(p, v); // Y is written once: do not displace the A panel
+      else *p = v;
+    };
     const unsigned lt0 = PAIR ? mapa(tempty_bar(0), 0) : tempty_bar(0);
     int it = 0;
     for (int t = unit; t < ntiles; t += nunits, ++it) {
@@ -450,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
           uint4* dst = (uint4*)((float*)P.Y + row * P.ldy + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            st_y(dst + j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
         } else {
           unsigned pk[16];
 #pragma unroll
@@ -462,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) ag_gemm_kernel(const __grid_const
           uint4* dst = (uint4*)((__nv_bfloat16*)P.Y + row * P.ldy + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            st_y(dst + j, make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
         }
       }
       tc_fence_before();
@@ -602,7 +631,7 @@ struct ag_gemm {
   int* h_err = nullptr;
   int* d_err = nullptr;
   int64_t opt_grid = 0, local_copy = 0, order = 0, group_m = 16, piece_kb = 64,
-          timeout_ms = 10000, comm = 1, pair = 1, stages = 6, opt_bn = 0;
+          timeout_ms = 10000, comm = 1, pair = 1, stages = 6, opt_bn = 0, l2hints = 0;
 };
 
 namespace {
@@ -912,6 +941,7 @@ int ag_gemm_forward(ag_gemm_t* h, const void* X, const void* w_local, void* Y, v
   P.piece_u4 = (long long)h->BN * h->K * 2 / 16 / h->pieces;
   P.comm = (h->W > 1 || h->local_copy) ? (int)h->comm : 0;
   P.local_copy = (int)h->local_copy;
+  P.l2hints = (int)h->l2hints;
   P.err = h->d_err;
   P.timeout_ns = h->timeout_ms * 1000000ll;
   const int grid = (int)grid_of(h);
@@ -944,6 +974,7 @@ int ag_gemm_set_option(ag_gemm_t* h, const char* key, int64_t v) {
   else if (k == "timeout_ms") { if (v < 1) return fail(h, 1, "timeout_ms >= 1"); h->timeout_ms = v; }
   else if (k == "comm") { if (v != 0 && v != 1) return fail(h, 1, "comm 0/1"); h->comm = v; }
   else if (k == "pair") { if (v != 0 && v != 1) return fail(h, 1, "pair 0/1"); h->pair = v; }
+  else if (k == "l2hints") { if (v < 0 || v > 7) return fail(h, 1, "l2hints: bit mask 0..7"); h->l2hints = v; }
   else if (k == "stages") { if (v != 6 && v != 7) return fail(h, 1, "stages 6/7"); h->stages = v; }
   else if (k == "bn") {
     if (v != 0 && v != 128 && v != 256) return fail(h, 1, "bn: 0 (auto), 128 or 256");
@@ -965,6 +996,7 @@ int ag_gemm_get_option(const ag_gemm_t* h, const char* key, int64_t* v) {
   else if (k == "timeout_ms") *v = h->timeout_ms;
   else if (k == "comm") *v = h->comm;
   else if (k == "pair") *v = h->pair;
+  else if (k == "l2hints") *v = h->l2hints;
   else if (k == "stages") *v = h->stages;
   else if (k == "bn") *v = h->opt_bn;
   else return 1;

@@ -59,16 +59,19 @@ def test_ablations_command_torchrun_shared_gpu():
     env = dict(os.environ, EMBA2A_SHARED_GPU="1")
     cmd = [sys.executable, os.path.join(ROOT, "tools", "ablations_torchrun.py"), "--gpus", "2",
            "--config", "tiny", "--slices", "4,32", "--ctas", "1", "--steps", "3", "--warmup", "3",
-           "--batches", "2", "--skew-us", "5"]
+           "--batches", "2", "--skew-us", "5", "--ag-config", "ag_tiny"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     recs = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
-    assert len(recs) == 2 + 1 + 6, r.stdout[-2000:]
+    assert len(recs) == 2 + 1 + 6 + 2, r.stdout[-2000:]
     for rec in recs:
         assert "error" not in rec, rec
-        assert rec["us_per_step"] > 0 and rec["parity"]["within_tol"] is True
+        if "AG" in rec["ablation"]:       # f4 points: TFLOP/s lines, oracle bound on every rank
+            assert rec["ms_per_step"] > 0 and rec["parity"]["within_bound"] is True
+        else:
+            assert rec["us_per_step"] > 0 and rec["parity"]["within_tol"] is True
     kinds = [next(iter(rec["ablation"])) for rec in recs]
-    assert kinds == ["E4", "E4", "E3"] + ["E5"] * 6
+    assert kinds == ["E4", "E4", "E3"] + ["E5"] * 6 + ["AG"] * 2
 
 
 @pytest.mark.gpu

@@ -9,6 +9,8 @@ and JSON line as the headline bench), printed as one JSON line with an "ablation
   E3  persistent CTAs per SM (occupancy vs memory contention)
   E5  comm-aware staggered / ascending / oblivious order, without and with a
       late rank (the last rank sleeps --skew-us on the GPU before each forward)
+  AG  the fused AllGather + GEMM: comm-aware tile order (own shard first, then
+      sources in arrival order) vs ascending source order, N > 1 only
 
 --gpus 1 runs bench.py directly (no peers: E5 is then meaningless and skipped).  With
 EMBA2A_SHARED_GPU=1 every rank shares cuda:0 (a test of the command, not a measurement).
@@ -34,7 +36,8 @@ def free_port():
 def run_point(args, extra, tag):
     base = [os.path.join(ROOT, "bench.py"), "--gpus", str(args.gpus), "--steps", str(args.steps),
             "--warmup", str(args.warmup), "--config", args.config, "--no-baseline",
-            "--no-backward", "--no-cpu", "--no-alpha0", "--batches", str(args.batches)] + extra
+            "--no-backward", "--no-cpu", "--no-alpha0", "--ag-leg", "0",
+            "--batches", str(args.batches)] + extra
     if args.gpus > 1:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
@@ -47,9 +50,12 @@ def run_point(args, extra, tag):
         rec = {"ablation": tag, "error": (r.stderr or r.stdout)[-1500:], "rc": r.returncode}
     else:
         d = json.loads(lines[0])
-        rec = {"ablation": tag, "n_gpus": d["n_gpus"], "us_per_step": d["us_per_step"],
+        rec = {"ablation": tag, "n_gpus": d["n_gpus"], "us_per_step": d.get("us_per_step"),
+               "ms_per_step": d.get("ms_per_step"),
                "value": d["value"], "unit": d["unit"], "roofline": d["roofline"],
                "parity": d.get("parity"), "clocks": d.get("clocks"), "config": d["config"]}
+        if "unfused" in d and "fused_speedup" in d["unfused"]:
+            rec["fused_speedup"] = d["unfused"]["fused_speedup"]
     print(json.dumps(rec), flush=True)
     if args.out:
         with open(args.out, "a") as f:
@@ -61,7 +67,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=8)
     ap.add_argument("--config", default="dlrm_small")
-    ap.add_argument("--which", default="E4,E3,E5")
+    ap.add_argument("--which", default="E4,E3,E5,AG")
+    ap.add_argument("--ag-config", default="ag_ffn")
     ap.add_argument("--slices", default="1,4,8,16,32,64,128,256")
     ap.add_argument("--ctas", default="1,2,3,4")
     ap.add_argument("--skew-us", type=float, default=20.0)
@@ -84,6 +91,11 @@ def main():
                 run_point(args, ["--order", str(order), "--skew-us", str(skew)],
                           {"E5": {"order": ["staggered", "ascending", "oblivious"][order],
                                   "skew_us_last_rank": skew}})
+    if "AG" in which and args.gpus > 1:
+        for order in (0, 1):
+            run_point(args, ["--path", "ag_gemm", "--ag-config", args.ag_config,
+                             "--ag-order", str(order)],
+                      {"AG": {"order": ["comm-aware", "ascending"][order]}})
 
 
 if __name__ == "__main__":

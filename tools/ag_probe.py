@@ -28,7 +28,12 @@ def t(steps=10):
     return a.elapsed_time(b) / steps
 flops = cfg.flops_per_rank()
 mode = sys.argv[2] if len(sys.argv) > 2 else "grid"
-if mode == "grid":
+if mode.startswith("grid_h"):                 # a few forwards with l2hints 0/1 (ncu target)
+    h.set_option("l2hints", int(mode[-1]))
+    for _ in range(6):
+        h.forward(X, Wr, Y)
+    torch.cuda.synchronize()
+elif mode == "grid":
     for pair in (1, 0):
         for grid in (148, 146, 144, 140, 128, 112, 96, 74, 64):
             h.set_option("pair", pair); h.set_option("grid", grid)
@@ -38,7 +43,8 @@ if mode == "grid":
 elif mode == "ab":
     # interleaved A/B: every config measured once per round, 5 rounds; min and median reported
     import statistics
-    confs = [dict(pair=1, stages=6, group_m=16), dict(pair=0, stages=6, group_m=16), "cublas"]
+    confs = [dict(pair=1, l2hints=0), dict(pair=1, l2hints=1), dict(pair=1, l2hints=4),
+             dict(pair=1, l2hints=5), dict(pair=1, l2hints=7), "cublas"]
     Yb = torch.empty_like(Y)
     res = {i: [] for i in range(len(confs))}
     for rnd in range(5):
