@@ -54,7 +54,7 @@ def run_point(args, extra, tag):
                "ms_per_step": d.get("ms_per_step"),
                "value": d["value"], "unit": d["unit"], "roofline": d["roofline"],
                "parity": d.get("parity"), "clocks": d.get("clocks"), "config": d["config"]}
-        if "unfused" in d and "fused_speedup" in d["unfused"]:
+        if isinstance(d.get("unfused"), dict) and "fused_speedup" in d["unfused"]:
             rec["fused_speedup"] = d["unfused"]["fused_speedup"]
     print(json.dumps(rec), flush=True)
     if args.out:
