@@ -112,7 +112,7 @@ def test_local_copy_single_rank():
     run_loopback(cfg_of(1, 128, 256, 128), opts={"local_copy": 1})
 
 
-@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("W", [2, 4, 8])
 def test_loopback_exact(W):
     flags = run_loopback(cfg_of(W, 256, 512, 512), forwards=1)
     # rank 0 received every remote chunk of epoch 1; its own row is never signalled
