@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--vec", type=int, default=0)
+    ap.add_argument("--opt", action="append", default=[],
+                    help="key=value library option for the fused op's handle (repeatable)")
     ap.add_argument("--order", type=int, default=-1)
     ap.add_argument("--ctas-per-sm", type=int, default=0, help="persistent grid per SM (E3)")
     ap.add_argument("--skew-us", type=float, default=0.0,
@@ -384,6 +386,9 @@ def main():
         h.set_option("order", args.order)
     if args.ctas_per_sm:
         h.set_option("ctas_per_sm", args.ctas_per_sm)
+    for kv in args.opt:
+        k_, v_ = kv.split("=")
+        h.set_option(k_, int(v_))
     ODT = {"f32": 0, "bf16": 1, "f16": 2}[args.out_dtype]
     oes = 4 if ODT == 0 else 2
     if ODT:
@@ -658,7 +663,7 @@ def main():
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
                    "order": h.get_option("order"), "ctas_per_sm": h.get_option("ctas_per_sm"),
-                   "chunk_bags": h.query("chunk_bags"),
+                   "chunk_bags": h.query("chunk_bags"), "opts": list(args.opt),
                    "skew_us_last_rank": args.skew_us,
                    "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
                           "distinct rows) over %.1f GB of tables, K back-to-back steps" %
