@@ -274,8 +274,14 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *                  look-back while the tiles fit one wave, else three kernels per pass,
  *                  reduce-then-scan), 1 always one kernel, 2 always three, 3 the segmented plan
  *                  (each table's lookups sorted by row bits only: 2 passes of <= 11-bit digits,
- *                  tiles aligned to tables; needs rows <= 2^22 and T <= 256, else as 0) --
+ *                  tiles aligned to tables; needs rows <= 2^22 and T <= 256, else as 0), 4 the
+ *                  cluster plan (ONE kernel: a thread-block cluster per table generates and
+ *                  sorts the table's lookups by row bits, <= 8-bit digits, digit offsets
+ *                  exchanged in distributed shared memory, passes split by cluster barriers) --
  *                  results identical in every mode
+ *   "cluster_ctas" cluster plan: CTAs per table cluster, 0 auto (default: the largest of 16, 8,
+ *                  4, 2 whose T clusters fit two CTAs per SM, else 1; smaller if the occupancy
+ *                  query says a cluster cannot be resident), or 1, 2, 4, 8, 16
  *   "bwd_threads"  backward kernel threads per CTA, multiple of 32 in [32, 128] (default 128;
  *                  the kernel is compiled with __launch_bounds__(128))
  *   "bwd_share"    divide the backward's persistent grid by this (default 1): W virtual ranks on

@@ -831,6 +831,368 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_seg_kernel(const Pa
   }
 }
 
+// ------------------------------------------------------------------- cluster sort plan
+// sort_mode 4: the whole plan in ONE kernel, one thread-block cluster of C CTAs per table.  The
+// input is table-major and the sort stable, so each table's segment is sorted by its row bits
+// alone (the segmented plan's observation) -- and a segment is small enough for one cluster to
+// own it, so the digit offsets of every pass are exchanged between the cluster's CTAs through
+// distributed shared memory and the passes are separated by cluster barriers: no global
+// look-back, no stamped words, no tile tickets and no kernel boundary between keygen and the
+// passes (the plain plan's 4 launches and their look-back round trips).
+//
+// CTA c of table t's cluster owns the strip of the segment made of bags
+// [t*B + c*B/C, t*B + (c+1)*B/C) (contiguous positions, strips in CTA order).  It generates those
+// keys (counting pass 0's digits as it goes), then in every pass: (1) counts its strip's digits,
+// (2) after a cluster barrier reads the C strips' counts (DSMEM) -- digit d of strip c starts at
+// seg_lo + (keys of the segment with a smaller digit) + (digit-d keys of strips 0..c-1) --
+// and (3) scatters its strip tile by tile in position order with the onesweep kernel's stable
+// warp-striped ranks; a cluster barrier (release/acquire at cluster scope: global stores too)
+// ends the pass.  Same key order as the plain plan, hence the same plan.
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// DPT consecutive 32-bit words at this CTA's shared address `addr`, read from cluster CTA `rank`
+template <int DPT>
+__device__ __forceinline__ void ld_dsmem(unsigned addr, unsigned rank, unsigned (&v)[DPT]) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(rank));
+  if constexpr (DPT == 1) {
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v[0]) : "r"(ra) : "memory");
+  } else if constexpr (DPT == 2) {
+    asm volatile("ld.shared::cluster.v2.u32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(ra)
+                 : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < DPT; k += 4)
+      asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[k]), "=r"(v[k + 1]), "=r"(v[k + 2]), "=r"(v[k + 3])
+                   : "r"(ra + 4u * k)
+                   : "memory");
+  }
+}
+
+// Exclusive scan of one value per thread over a block of NW warps.
+template <int NW>
+__device__ __forceinline__ unsigned block_excl_scan_nw(unsigned v, unsigned* s_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  unsigned base = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) base += i < w ? s_warp[i] : 0u;
+  __syncthreads();                     // s_warp may be reused right after
+  return base + x - v;
+}
+
+// Per-CTA timeline of the cluster plan (the "trace" option): events 40 start, 41 keys generated,
+// then per pass (payload = pass) 43 the pass's counts complete (cluster barrier), 44 offsets
+// known, 45 strip written; 46 the cluster done.  Thread 0 only.
+__device__ __forceinline__ void ctrace(const ClusterSortParams& S, unsigned event, unsigned payload) {
+  if (S.trace == nullptr || threadIdx.x != 0) return;
+  const unsigned long long i = atomicAdd(S.trace, 1ull);
+  if ((long long)i >= S.trace_cap) return;
+  S.trace[2 + 2 * i] = ((unsigned long long)blockIdx.x << 40) |
+                       ((unsigned long long)event << 32) | payload;
+  S.trace[3 + 2 * i] = globaltimer();
+}
+
+// One CTA = kClThreads threads; a tile = kClThreads * kClItems positions, warp w owning
+// [w*32*I, (w+1)*32*I) of it, item i of lane l at w*32*I + i*32 + l (warp-striped: "item, then
+// lane" is position order, so the match.any ranks are stable).  A pass over the strip, tile by
+// tile: rank (per-warp digit counts), reorder the tile by digit in shared memory, write each
+// digit's run out contiguously (coalesced; a 4-byte scatter per key costs the SM one L2 sector
+// per key: measured 4-5 us per pass for ~2.5 K keys per CTA), and -- while writing -- count the
+// NEXT pass's digit of every key into the counts of the CTA whose strip the key lands in
+// (red.shared::cluster), so a pass needs one cluster barrier and no counting sweep.  Counts
+// rotate over three buffers: pass p reads buffer p%3, its write-out adds to (p+1)%3, and
+// (p+2)%3 -- last read in pass p-1, next written in pass p+1 -- is zeroed during pass p.
+constexpr int kClThreads = 256;
+constexpr int kClItems = 12;
+constexpr int kClTile = kClThreads * kClItems;
+constexpr int kClMaxC = 16;
+size_t cluster_smem(int db, bool weights) {
+  const size_t ND = (size_t)1 << (db <= 8 ? 8 : db);
+  return ND * 4 * 6 + (size_t)(kClThreads / 32) * ND * 2 + (size_t)kClTile * (weights ? 12 : 8);
+}
+template <bool WEIGHTED, int DB>
+__global__ void __launch_bounds__(kClThreads, 2) bwd_cluster_sort_kernel(const ClusterSortParams S) {
+  constexpr int ND = 1 << DB, NW = kClThreads / 32, K = kClItems, TILE = kClTile;
+  constexpr int DPT = ND / kClThreads, BPW = 32;
+  static_assert(DPT >= 1 && DPT <= 8, "1..8 digits per thread");
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* s_hist = reinterpret_cast<unsigned*>(smem);   // [3][ND] strip digit counts (cluster)
+  unsigned* s_run = s_hist + 3 * ND;                      // [ND] next output slot per digit
+  unsigned* s_tstart = s_run + ND;                        // [ND] first tile slot per digit
+  unsigned* s_gofs = s_tstart + ND;                       // [ND] output slot of the tile's run
+  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(s_gofs + ND);   // [NW][ND]
+  unsigned* s_key = reinterpret_cast<unsigned*>(s_cnt + NW * ND);          // [TILE]
+  int* s_bag = reinterpret_cast<int*>(s_key + TILE);                       // [TILE]
+  float* s_wt = reinterpret_cast<float*>(s_bag + TILE);                    // [TILE] (weighted)
+  __shared__ unsigned s_warp[NW];
+  __shared__ unsigned s_sb[kClMaxC + 1];                  // strip starts of the cluster's CTAs
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned C = (unsigned)S.C, c = cluster_ctarank();
+  const long long t = blockIdx.x / S.C;
+  for (int i = tid; i < 3 * ND; i += kClThreads) s_hist[i] = 0u;
+  for (int i = tid; i < NW * ND / 2; i += kClThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
+  pdl_wait();     // the caller's indices/offsets and the previous plan's readers are complete
+  pdl_trigger();
+  if (tid <= (int)C) s_sb[tid] = (unsigned)S.offsets[t * S.B + ((long long)tid * S.B) / C];
+  const long long jlo = t * S.B + ((long long)c * S.B) / C;
+  const long long jhi = t * S.B + ((long long)(c + 1) * S.B) / C;
+  const long long seg_lo = S.offsets[t * S.B];
+  const long long s0 = S.offsets[jlo], s1 = S.offsets[jhi];
+  const unsigned mask0 = S.passes > 0 ? (1u << min(S.db, S.rbits)) - 1u : 0u;
+  ctrace(S, 40, 0);
+  // (every CTA's count buffers are zeroed above, before its pass-0 barrier; remote adds start
+  // after that barrier)
+  // ---- keygen over this strip's bags: a warp takes 32 bags (one offset per lane), walks their
+  //      lookups UNROLL x 32 at a time, finds each lookup's bag by a 5-step search over the
+  //      lanes' offsets; pass 0's digit counts on the side
+  {
+    unsigned* const keys = S.keys[0];
+    int* const bags = S.bags[0];
+    float* const wts = S.wts[0];
+    for (long long b0 = jlo + (long long)w * BPW; b0 < jhi; b0 += (long long)NW * BPW) {
+      const int nb = (jhi - b0) < BPW ? (int)(jhi - b0) : BPW;
+      const int my_off = lane < nb ? S.offsets[b0 + lane] : 0x7fffffff;
+      const int lo = __shfl_sync(kFull, my_off, 0);
+      const int hi = S.offsets[b0 + nb];
+      constexpr int UNROLL = 12;
+      for (int base0 = lo; base0 < hi; base0 += 32 * UNROLL) {
+        int ix[UNROLL];
+        float wv[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const int p = base0 + 32 * u + lane;
+          ix[u] = p < hi ? S.indices[p] : 0;
+          if (WEIGHTED) wv[u] = p < hi ? S.weights[p] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const int p = base0 + 32 * u + lane;
+          if (base0 + 32 * u >= hi) break;            // warp-uniform
+          int i = 0;
+#pragma unroll
+          for (int step = BPW / 2; step >= 1; step >>= 1) {
+            const int v = __shfl_sync(kFull, my_off, i + step);
+            if (i + step < nb && v <= p) i += step;
+          }
+          const unsigned row = (unsigned)ix[u];
+          unsigned d = (unsigned)ND;                   // invalid: counted nowhere
+          if (p < hi) {
+            const long long bag = b0 + i;
+            keys[p] = ((unsigned)(bag / S.B) << S.rbits) | row;
+            bags[p] = (int)bag;
+            if (WEIGHTED) wts[p] = wv[u];
+            d = row & mask0;
+          }
+          const unsigned peers = __match_any_sync(kFull, d);
+          if (d < (unsigned)ND && lane == __ffs(peers) - 1) atomicAdd(&s_hist[d], __popc(peers));
+        }
+      }
+    }
+  }
+  ctrace(S, 41, 0);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const long long wbase = (long long)w * (32 * K);
+  for (int p = 0; p < S.passes; ++p) {
+    const int shift = p * S.db;
+    const unsigned dmask = (1u << min(S.db, S.rbits - shift)) - 1u;
+    const bool last = p == S.passes - 1;
+    const int shift2 = shift + S.db;
+    const unsigned dmask2 = last ? 0u : (1u << min(S.db, S.rbits - shift2)) - 1u;
+    const bool odd = p & 1;            // (selects, not indexing: keeps the params in registers)
+    const unsigned* const kin = odd ? S.keys[1] : S.keys[0];
+    const int* const bin = odd ? S.bags[1] : S.bags[0];
+    const float* const win = odd ? S.wts[1] : S.wts[0];
+    unsigned* const kout = odd ? S.keys[0] : S.keys[1];
+    int* const bout = odd ? S.bags[0] : S.bags[1];
+    float* const wout = odd ? S.wts[0] : S.wts[1];
+    unsigned* const h_cur = s_hist + (p % 3) * ND;
+    const unsigned h_next = smem_u32(s_hist + ((p + 1) % 3) * ND);
+    cluster_barrier();                 // counts of this pass complete; pass p-1's keys in place
+    ctrace(S, 43, p);
+    {
+      unsigned* const h_free = s_hist + ((p + 2) % 3) * ND;   // read in pass p-1, written in p+1
+      for (int i = tid; i < ND; i += kClThreads) h_free[i] = 0u;
+    }
+    // digit offsets: thread tid owns digits tid*DPT .. +DPT-1 and reads their counts in every
+    // strip of the cluster (DSMEM)
+    {
+      unsigned tot[DPT], bef[DPT];
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) tot[k] = bef[k] = 0u;
+      const unsigned a = smem_u32(h_cur + tid * DPT);
+#pragma unroll 4
+      for (unsigned q = 0; q < C; ++q) {
+        unsigned v[DPT];
+        ld_dsmem<DPT>(a, q, v);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+          tot[k] += v[k];
+          if (q < c) bef[k] += v[k];
+        }
+      }
+      block_excl_scan_dpt<DPT>(tot, s_warp);
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) s_run[tid * DPT + k] = (unsigned)seg_lo + tot[k] + bef[k];
+    }
+    __syncthreads();
+    ctrace(S, 44, p);
+    for (long long base = s0; base < s1; base += TILE) {
+      unsigned key[K], dg[K];
+      int bag[K];
+      float wt[K];
+      unsigned short rank[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const long long pos = base + wbase + i * 32 + lane;
+        const bool valid = pos < s1;
+        key[i] = valid ? __ldcg(kin + pos) : 0u;
+        bag[i] = valid ? __ldcg(bin + pos) : 0;
+        if (WEIGHTED) wt[i] = valid ? __ldcg(win + pos) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const long long pos = base + wbase + i * 32 + lane;
+        dg[i] = pos < s1 ? ((key[i] >> shift) & dmask) : (unsigned)ND;
+        if (base + wbase + i * 32 >= s1) continue;     // warp-uniform
+        const unsigned peers = __match_any_sync(kFull, dg[i]);
+        const unsigned cur = dg[i] < (unsigned)ND ? s_cnt[w * ND + dg[i]] : 0u;
+        rank[i] = (unsigned short)(cur + __popc(peers & lt_mask));
+        __syncwarp();
+        if (dg[i] < (unsigned)ND && lane == __ffs(peers) - 1)
+          s_cnt[w * ND + dg[i]] = (unsigned short)(cur + __popc(peers));
+        __syncwarp();
+      }
+      __syncthreads();
+      {                                // per digit: warp offsets, tile start, output slot
+        unsigned cnt[DPT];
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+          const int d = tid * DPT + k;
+          unsigned acc = 0;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) {
+            const unsigned x = s_cnt[ww * ND + d];
+            s_cnt[ww * ND + d] = (unsigned short)acc;
+            acc += x;
+          }
+          cnt[k] = acc;
+        }
+        unsigned st[DPT];
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) st[k] = cnt[k];
+        block_excl_scan_dpt<DPT>(st, s_warp);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+          const int d = tid * DPT + k;
+          s_tstart[d] = st[k];
+          s_gofs[d] = s_run[d];
+          s_run[d] += cnt[k];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (dg[i] >= (unsigned)ND) continue;
+        const unsigned lp = s_tstart[dg[i]] + s_cnt[w * ND + dg[i]] + rank[i];
+        s_key[lp] = key[i];
+        s_bag[lp] = bag[i];
+        if (WEIGHTED) s_wt[lp] = wt[i];
+      }
+      __syncthreads();
+      const int tn = (s1 - base) < TILE ? (int)(s1 - base) : TILE;
+      for (int i0 = 0; i0 < tn; i0 += kClThreads) {
+        const int i = i0 + tid;
+        unsigned k2 = (unsigned)ND, q = 0u;
+        if (i < tn) {
+          const unsigned k = s_key[i];
+          const unsigned dd = (k >> shift) & dmask;
+          const unsigned out = s_gofs[dd] + (unsigned)i - s_tstart[dd];
+          kout[out] = k;
+          bout[out] = s_bag[i];
+          if (WEIGHTED) wout[out] = s_wt[i];
+          if (!last) {                 // the next pass's digit, counted at the strip it lands in
+            unsigned lo = 0u;
+#pragma unroll
+            for (unsigned stp = kClMaxC / 2; stp >= 1; stp >>= 1)
+              if (lo + stp < C && s_sb[lo + stp] <= out) lo += stp;
+            q = lo;
+            k2 = (k >> shift2) & dmask2;
+          }
+        }
+        if (!last) {
+          const unsigned tag = k2 < (unsigned)ND ? (q << 16) | k2 : 0xffffffffu;
+          const unsigned peers = __match_any_sync(kFull, tag);
+          if (tag != 0xffffffffu && lane == __ffs(peers) - 1) {
+            unsigned ra;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(ra) : "r"(h_next + 4u * k2), "r"(q));
+            asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(ra), "r"(__popc(peers))
+                         : "memory");
+          }
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < NW * ND / 2; i += kClThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
+      __syncthreads();
+    }
+    ctrace(S, 45, p);
+  }
+  cluster_barrier();                   // no CTA leaves while a peer may still read its counts
+  ctrace(S, 46, 0);
+}
+
+template <bool W, int DB>
+const void* cluster_fn() {
+  return reinterpret_cast<const void*>(bwd_cluster_sort_kernel<W, DB>);
+}
+const void* pick_cluster_fn(int db, bool weights) {
+  switch (db <= 8 ? 8 : db) {
+    case 8: return weights ? cluster_fn<true, 8>() : cluster_fn<false, 8>();
+    case 9: return weights ? cluster_fn<true, 9>() : cluster_fn<false, 9>();
+    case 10: return weights ? cluster_fn<true, 10>() : cluster_fn<false, 10>();
+    case 11: return weights ? cluster_fn<true, 11>() : cluster_fn<false, 11>();
+    default: return nullptr;
+  }
+}
+cudaLaunchConfig_t cluster_cfg(int T, int C, size_t sm, cudaStream_t st, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(T * C));
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cfg;
+}
+cudaError_t prep_cluster_fn(const void* fn, size_t sm) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
 // ------------------------------------------------------------------------- fused backward
 // Per-warp timeline of the backward (the "trace" option; read with emb_a2a_read_trace): record
 // (warp << 40 | event << 32 | payload, %globaltimer).  Events: 20 warp start, 21 exchange done,
@@ -1508,6 +1870,43 @@ cudaError_t launch_sort_plan_seg(const SortParams& S, const PassParams* passes, 
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+
+int cluster_plan_size(int T, int db, bool weights) {
+  const void* fn = pick_cluster_fn(db, weights);
+  const size_t sm = cluster_smem(db, weights);
+  if (!fn || T <= 0 || prep_cluster_fn(fn, sm) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int C = 16; C >= 1; C >>= 1) {
+    // the largest cluster whose T copies fit two CTAs per SM (1 if even that is short)
+    if (C > 1 && (long long)T * C > 2LL * sms) continue;
+    cudaLaunchAttribute attr[2];
+    cudaLaunchConfig_t cfg = cluster_cfg(T, C, sm, 0, attr);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0) return C;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+cudaError_t launch_sort_plan_cluster(const ClusterSortParams& S, int T, cudaStream_t st) {
+  if (T <= 0 || S.B <= 0) return cudaSuccess;
+  const void* fn = pick_cluster_fn(S.db, S.weights != nullptr);
+  if (!fn) return cudaErrorInvalidValue;
+  const size_t sm = cluster_smem(S.db, S.weights != nullptr);
+  cudaError_t e = prep_cluster_fn(fn, sm);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  cudaLaunchConfig_t cfg = cluster_cfg(T, S.C, sm, st, attr);
+  ClusterSortParams s = S;
+  void* args[] = {&s};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // Persistent grid: every CTA must be resident at once (the exchange wait and the chunk fold

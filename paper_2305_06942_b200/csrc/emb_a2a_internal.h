@@ -232,6 +232,29 @@ struct PassParams {
   const unsigned* shist;       // this pass's [T][NB] per-table digit counts
 };
 
+// Cluster plan (sort_mode 4): one thread-block cluster of C CTAs per table generates the keys of
+// the table's segment and sorts it by row bits (every LSD pass in one kernel; digit offsets
+// exchanged through distributed shared memory, passes separated by cluster barriers).
+constexpr int kClusterMaxDB = 11;              // digit bits per pass
+struct ClusterSortParams {
+  const int* indices;
+  const int* offsets;          // absolute CSR offsets [T*B + 1]; table t = [offsets[t*B], ..)
+  const float* weights;        // NULL = unweighted
+  unsigned* keys[2];           // ping-pong: keygen writes [0]; pass p reads [p&1], writes [p+1&1]
+  int* bags[2];
+  float* wts[2];
+  long long B;
+  int C;                       // CTAs per cluster (= per table)
+  int rbits;                   // row bits (key = t << rbits | row)
+  int passes;                  // LSD passes over the row bits (0 when every row is 0)
+  int db;                      // digit bits per pass (the last pass may be narrower)
+  unsigned long long* trace;   // optional %globaltimer event log (the "trace" option), NULL = off
+  long long trace_cap;
+};
+cudaError_t launch_sort_plan_cluster(const ClusterSortParams& S, int T, cudaStream_t st);
+// CTAs per cluster the cluster plan would use for T tables (0 = cannot launch)
+int cluster_plan_size(int T, int db, bool weights);
+
 // The fused backward (exchange + reduce + update) and the unfused reduce share one kernel.
 struct BwdParams {
   const float* grad;           // fused: own [b_r][G*D] output gradient; local: [B][T][D] (MP)

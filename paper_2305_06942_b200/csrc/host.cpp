@@ -138,6 +138,7 @@ struct emb_a2a {
 
   // backward (f3)
   int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0, sort_stall = 0;
+  int64_t cluster_ctas = 0;              // cluster plan: CTAs per table (0 auto)
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
   unsigned long long* bflags = nullptr;  // own backward arrival counters
@@ -1215,6 +1216,46 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     CUDA_TRY(h, cudaMemsetAsync(h->d_hist, 0, 2 * kHistWords * sizeof(unsigned), st));
     if (h->d_shist) CUDA_TRY(h, cudaMemsetAsync(h->d_shist, 0, 2 * h->shist_half * 4, st));
   }
+  // Cluster plan (sort_mode 4, backward.cu "cluster sort plan"): keygen + every pass in one
+  // kernel, one thread-block cluster per table, digit offsets exchanged in distributed shared
+  // memory.  Needs the table-major segments of an in-range key (checked above).
+  if (h->sort_mode == 4 && n > 0) {
+    const int cpasses = rbits == 0 ? 0 : (rbits + kClusterMaxDB - 1) / kClusterMaxDB;
+    const int cdb = cpasses ? (rbits + cpasses - 1) / cpasses : 0;
+    const int C = h->cluster_ctas > 0 ? (int)h->cluster_ctas : cluster_plan_size(h->T, cdb, wtd);
+    if (C <= 0) return fail(h, EMB_A2A_ECUDA, "backward cluster plan: no cluster size fits");
+    ClusterSortParams cs;
+    memset(&cs, 0, sizeof(cs));
+    cs.indices = indices;
+    cs.offsets = offsets;
+    cs.weights = wtd ? weights : nullptr;
+    for (int x = 0; x < 2; ++x) {
+      cs.keys[x] = h->d_keys[x];
+      cs.bags[x] = h->d_bags[x];
+      cs.wts[x] = wtd ? h->d_wts[x] : nullptr;
+    }
+    cs.B = h->B;
+    cs.C = C;
+    cs.rbits = rbits;
+    cs.passes = cpasses;
+    cs.db = cdb;
+    cs.trace = h->d_trace;
+    cs.trace_cap = h->trace_cap;
+    h->planned = false;
+    cudaError_t e = launch_sort_plan_cluster(cs, h->T, st);
+    if (e != cudaSuccess)
+      return fail(h, EMB_A2A_ECUDA, "backward cluster plan launch (C=%d): %s", C,
+                  cudaGetErrorString(e));
+    h->plan_no += 1;
+    h->rbits = rbits;
+    h->plan_weighted = wtd;
+    h->plan_offsets = offsets;
+    h->plan_n = n;
+    h->plan_buf = cpasses & 1;
+    h->planned = true;
+    h->kernel_launches += 1;
+    return EMB_A2A_OK;
+  }
   h->plan_no += 1;
   h->rbits = rbits;
   h->plan_weighted = wtd;
@@ -1475,8 +1516,12 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (v < -1 || v > 1) return fail(h, EMB_A2A_EINVAL, "debug_credit_lag in {-1, 0, 1}");
     h->credit_lag_opt = v;
   } else if (k == "sort_mode") {
-    if (v < 0 || v > 3) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3}");
+    if (v < 0 || v > 4) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3, 4}");
     h->sort_mode = v;
+  } else if (k == "cluster_ctas") {
+    if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16)
+      return fail(h, EMB_A2A_EINVAL, "cluster_ctas in {0 (auto), 1, 2, 4, 8, 16}");
+    h->cluster_ctas = v;
   } else if (k == "bwd_threads") {
     // bwd_kernel is compiled with __launch_bounds__(128, ...): more threads cannot launch
     if (v < 32 || v > 128 || v % 32) return fail(h, EMB_A2A_EINVAL, "bwd_threads: 32..128, x32");
@@ -1520,6 +1565,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "pdl_rows_early") *v = h->rows_early;
   else if (k == "debug_credit_lag") *v = h->credit_lag_opt;
   else if (k == "sort_mode") *v = h->sort_mode;
+  else if (k == "cluster_ctas") *v = h->cluster_ctas;
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;

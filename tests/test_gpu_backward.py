@@ -586,3 +586,137 @@ def test_segmented_plan_stall_reports_timeout():
         h.check()
     assert "ETIMEOUT" in str(e.value)
     h.destroy()
+
+
+# ------------------------------------------------------------------ cluster plan (sort_mode 4)
+
+@pytest.mark.parametrize("ctas", [0, 1, 4, 16])
+@pytest.mark.parametrize("seed,W,weighted", [(0, 1, False), (1, 1, True), (2, 2, False),
+                                             (3, 4, False), (4, 2, True)])
+def test_cluster_plan_exact_vs_oracle(seed, W, weighted, ctas):
+    """The cluster plan (sort_mode 4: one kernel, a thread-block cluster per table, keygen and
+    every row-digit pass, offsets exchanged in distributed shared memory) gives the oracle's
+    tables bitwise in exact-int mode, at every cluster size (strips of 1..16 CTAs per table)."""
+    p, w = _seg_problem(7300 + seed, W, weighted)
+    grads = grads_for(p, seed, 1)
+    kw = {} if w is None else {"weights": w}
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 0.5, **kw)
+    run = Run(p, opts={"sort_mode": 4, "cluster_ctas": ctas})
+    run.backward(grads, 0.5, weights=w)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+@pytest.mark.parametrize("seed,W,weighted,rows", [(0, 1, False, (1 << 16, 1 << 18)),
+                                                  (1, 1, True, (1 << 18, 1 << 20)),
+                                                  (2, 2, False, (1 << 20, 1 << 22)),
+                                                  (3, 1, False, (1 << 21, 1 << 22)),
+                                                  (4, 1, False, (1 << 8, 1 << 9)),
+                                                  (5, 1, True, (1 << 11, 1 << 12))])
+def test_cluster_plan_equals_plain_plan_digit_widths(seed, W, weighted, rows):
+    """9..22 row bits (2 passes of 5-bit digits .. 3 passes of 8): the cluster plan gives the
+    plain (table, row) plan's order, so the updated tables are bitwise those of sort_mode 1
+    (fp32 values: any other order would change the rounding somewhere)."""
+    p, w = _seg_problem(7350 + seed, W, weighted, rows)
+    grads = grads_for(p, seed, 0)
+    outs = []
+    for mode in (1, 4):
+        run = Run(p, opts={"sort_mode": mode})
+        run.backward(grads, 0.5, weights=w)
+        outs.append(run.tables())
+        run.destroy()
+    for a, b in zip(outs[1], outs[0]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", ["one_row", "tiny_batch", "empty_bags", "one_table", "mean"])
+def test_cluster_plan_degenerate(case):
+    """Edge cases of the cluster plan vs the oracle (exact-int): every row 0 (no radix pass at
+    all: keygen only), fewer bags than cluster CTAs (empty strips), mostly empty bags, a single
+    table (one cluster), and mean pooling (per-bag division in pass 1)."""
+    rng = np.random.default_rng(77)
+    D, T, R, B, maxL = 8, 3, 500, 256, 12
+    pooling = "sum"
+    if case == "one_row":
+        R = 1
+    elif case == "tiny_batch":
+        B = 3
+    elif case == "empty_bags":
+        maxL = 1
+    elif case == "one_table":
+        T = 1
+    elif case == "mean":
+        pooling = "mean"
+    tables = [rng.integers(-8, 8, (R, D)).astype(np.float32) for _ in range(T)]
+    bags = [[list(rng.integers(0, R, rng.integers(0, maxL + 1))) for _ in range(B)] for _ in range(T)]
+    i, o = csr_from_bags(bags)
+    p = Problem(1, [T], D, B, np.array([0, B]), tables, [i], [o])
+    grads = grads_for(p, 3, 1)
+    kw = {"pooling": oracle.MEAN} if pooling == "mean" else {}
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 0.5, **kw)
+    run = Run(p, pooling=pooling, opts={"sort_mode": 4, "cluster_ctas": 16})
+    run.backward(grads, 0.5)
+    got = run.tables()
+    run.destroy()
+    if pooling == "mean":
+        bound_check(p, got, want, grads, 0.5, pooling=oracle.MEAN)
+    else:
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_cluster_plan_switching_plan_kinds():
+    """Cluster, plain and segmented plans in any order on one handle: the plain plans' two
+    digit-count halves (each keygen zeroing the other) are untouched by the cluster plan, so
+    every backward still matches the oracle bitwise for the plan it follows."""
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    rng = np.random.default_rng(6)
+    D, B, T, R = 8, 512, 4, 3000
+    tab0 = [rng.integers(-8, 8, (R, D)).astype(np.float32) for _ in range(T)]
+    h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0))
+    tabs = [torch.from_numpy(t).to(dev()) for t in tab0]
+    h.register_tables(tabs, B)
+    want = [t.copy() for t in tab0]
+    for step, mode in enumerate([4, 0, 4, 4, 3, 4, 1, 0, 4]):
+        bags = [[list(rng.integers(0, R, rng.integers(0, 30))) for _ in range(B)] for _ in range(T)]
+        i, o = csr_from_bags(bags)
+        h.set_option("sort_mode", mode)
+        h.backward_plan(torch.from_numpy(i).to(dev()), torch.from_numpy(o).to(dev()))
+        grad = rng.integers(-4, 4, (B, T * D)).astype(np.float32)
+        h.backward(torch.from_numpy(grad).to(dev()), 0.5)
+        want = oracle.backward_sgd([0, B], D, B, [T], want, [i], [o], [grad], 0.5)
+        torch.cuda.synchronize()
+        h.check()
+        for a, b in zip(tabs, want):
+            np.testing.assert_array_equal(a.cpu().numpy(), b, err_msg=f"step {step} mode {mode}")
+    h.destroy()
+
+
+@pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p8", "dlrm_wide"])
+def test_cluster_plan_full_size_equals_plain(name):
+    """BASELINE configs at full size (W=1 per-rank work): the cluster plan's tables are bitwise
+    those of the plain plan (fp32 gradients, so equal results need the same lookup order; the
+    plain plan is pinned to the oracle on sampled rows by test_full_size_backward_sampled_rows)."""
+    cfg = synth.config_for(name, W=1)
+    idx_h, off_h = synth.gen_all_csr(cfg, 0)[0]
+    rng = np.random.default_rng(1)
+    grad = torch.from_numpy(rng.standard_normal((cfg.B, cfg.G * cfg.D)).astype(np.float32)).to(dev())
+    idx = torch.from_numpy(idx_h).to(dev())
+    off = torch.from_numpy(off_h).to(dev())
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    outs = []
+    for mode in (0, 4):
+        h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0), {"sort_mode": mode})
+        tabs = [torch.zeros(cfg.R, cfg.D, device=dev()) for _ in range(cfg.T[0])]
+        h.register_tables(tabs, cfg.B)
+        h.backward_plan(idx, off)
+        h.backward(grad, -1.0)
+        torch.cuda.synchronize()
+        h.check()
+        outs.append(tabs)
+        h.destroy()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    del outs
+    torch.cuda.empty_cache()
