@@ -77,6 +77,7 @@ struct KParams {
                       // only by exiting)
   int credit_lag;     // a peer's credit must reach epoch - credit_lag before we store into it
   int flat_below;     // stages whose average bag length is below this use row-flattened pooling
+  int l1rows;         // fp32 unweighted LSU gathers: rows allocated in L1 (instance set ELEM 3)
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
   int chunk_base[kMaxW + 1];    // first chunk of destination ordinal k; [W] = nchunks
@@ -126,6 +127,15 @@ __host__ __device__ inline void slice_of_chunk(const KParams& P, int k, int s, i
   slice_bags = rem < P.S ? (int)rem : P.S;
 }
 
+// fp32 rows are gathered through L1 (auto "l1_rows") for forwards with at least kL1RowsPerSm
+// lookups per SM or at least kL1RowsBags bags per table: a Zipf-hot row then recurs on the same
+// SM often enough that L1 hits beat streaming every row past L1.  Measured (r02ak, W=1, on vs
+// off): DLRM-wide 193 -> 162 us, sweep P=32 155.5 -> 133.7, P=8 62.9 -> 59.5, P=4 41.1 -> 38.7,
+// P=1 22.6 -> 22.0 (B = 4096 / 8192); DLRM-small 12.4 -> 12.7 and weak 18.8 -> 19.6 (B = 2048 /
+// 1024, ~2.2 K lookups per SM) -- left streaming.
+constexpr long long kL1RowsPerSm = 4096;
+constexpr long long kL1RowsBags = 4096;
+
 // Fill stage_bytes / payload_off / payload_cap for P.tma, P.C, P.D4 (kernels.cu).
 void stage_layout(KParams& P, int stage_kb, int idx_cap);
 
@@ -151,6 +161,7 @@ cudaError_t plan_fused(const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
 cudaError_t plan_with(const void* fn, const KParams& P, const LaunchCfg& c, LaunchPlan* pl);
 cudaError_t plan_f32(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
 cudaError_t plan_f32w(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
+cudaError_t plan_f32l1(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
 cudaError_t plan_bf16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,
                       LaunchPlan* pl);
 cudaError_t plan_f16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,

@@ -126,13 +126,22 @@ __device__ __forceinline__ float4 ld_row4_pred(const float4* p, bool pred) {
 }
 
 // Predicated 16-byte raw load ("unit"): when !pred the destination is all-zero bits, which is +0.0
-// in every element type (no memory access).
+// in every element type (no memory access).  L1 = false: L1::no_allocate (streams past L1); L1 =
+// true: the row is allocated in L1, so a hot (Zipf head) row gathered again by the same SM is
+// served there instead of queueing on its L2 slice (the fp32 "L1 rows" instance set, ELEM 3).
+template <bool L1>
 __device__ __forceinline__ uint4 ld_unit_pred(const uint4* p, bool pred) {
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "l"(p), "r"((int)pred));
+  if constexpr (L1)
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"((int)pred));
+  else
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"((int)pred));
   return v;
 }
 
@@ -142,16 +151,17 @@ __device__ __forceinline__ float lds_f32(unsigned addr) {
   return v;
 }
 
-// Table element types: 0 = fp32 (4 per 16-byte unit), 1 = bf16, 2 = fp16 (8 per unit).  Every
-// element is converted EXACTLY to fp32 before it is accumulated (R#28).
+// Table element types: 0 = fp32 (4 per 16-byte unit), 1 = bf16, 2 = fp16 (8 per unit); 3 = fp32
+// with L1-allocating row loads (ld_unit_pred).  Every element is converted EXACTLY to fp32 before
+// it is accumulated (R#28).
 template <int ELEM>
 struct Elem {
-  static constexpr int EPU = ELEM == 0 ? 4 : 8;
+  static constexpr int EPU = (ELEM == 0 || ELEM == 3) ? 4 : 8;
 };
 
 template <int ELEM>
 __device__ __forceinline__ void unit_to_f(const uint4& u, float (&f)[Elem<ELEM>::EPU]) {
-  if constexpr (ELEM == 0) {
+  if constexpr (ELEM == 0 || ELEM == 3) {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
     f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
   } else if constexpr (ELEM == 1) {   // bf16 = top half of binary32
@@ -280,7 +290,7 @@ __device__ __forceinline__ void pool_bag_lsu(const uint4* __restrict__ tab, int 
     for (int u = 0; u < U; ++u) {
       const uint4* r = tab + (size_t)(unsigned)row[u] * DU + lane;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred(r + v * LPB, colok[v] && (u < n));
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<ELEM == 3>(r + v * LPB, colok[v] && (u < n));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -367,7 +377,7 @@ __device__ __forceinline__ void pool_run_lsu(const uint4* __restrict__ tab, int 
     for (int u = 0; u < U; ++u) {
       const uint4* r = tab + (size_t)(unsigned)row[u] * DU + lane;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred(r + v * LPB, colok[v] && (u < n));
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<ELEM == 3>(r + v * LPB, colok[v] && (u < n));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -923,7 +933,7 @@ KernelFn pick_lpb(int DU, bool tma) {
 // fp32 tables: NV in {1,2,4,8} (D <= 1024); 16-bit tables: NV in {1,2,4} (8 elements per unit)
 template <int ELEM, bool FUSED, bool WEIGHTED>
 KernelFn pick(int DU, int nv_want, bool tma) {
-  constexpr int kMaxNV = ELEM == 0 ? 8 : 4;
+  constexpr int kMaxNV = (ELEM == 0 || ELEM == 3) ? 8 : 4;
   switch (choose_nv(DU, nv_want, kMaxNV)) {
     case 1: return pick_lpb<ELEM, 1, FUSED, WEIGHTED>(DU, tma);
     case 2: return pick_lpb<ELEM, 2, FUSED, WEIGHTED>(DU, tma);

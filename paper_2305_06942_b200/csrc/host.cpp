@@ -131,6 +131,9 @@ struct emb_a2a {
   int slice_base[kMaxW + 1] = {0};
   int chunk_base[kMaxW + 1] = {0};
   int C = 8, nchunks = 0;
+  int64_t l1_opt = -1;                   // "l1_rows": -1 auto (kL1RowsPerSm), 0 off, 1 on
+  int l1_cur = 0;                        // this chunk plan's choice
+  int sms = 0;
   int last_grid = 0;
   LaunchPlan plan_fused[2], plan_pool[2]; // cached launch configurations [weighted]
                                           // (fn == nullptr: stale)
@@ -335,8 +338,13 @@ void compute_slices(emb_a2a* h, int C) {
 // cached launch configurations depend on it: grid = min(slots, chunks), stage layout).
 void ensure_chunk(emb_a2a* h, int64_t nnz) {
   const int C = h->chunk > 0 ? chunk_size(h->S, h->chunk) : auto_chunk(h, nnz);
-  if (C == h->C) return;
-  compute_slices(h, C);
+  if (h->sms <= 0) cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
+  const int l1 = h->l1_opt >= 0 ? (int)h->l1_opt
+                                : ((nnz >= kL1RowsPerSm * std::max(h->sms, 1) ||
+                                    (long long)h->B >= kL1RowsBags) ? 1 : 0);
+  if (C == h->C && l1 == h->l1_cur) return;
+  h->l1_cur = l1;
+  if (C != h->C) compute_slices(h, C);
   for (int w = 0; w < 2; ++w) {
     h->plan_fused[w] = LaunchPlan();
     h->plan_pool[w] = LaunchPlan();
@@ -395,6 +403,7 @@ KParams make_params(emb_a2a* h, const int32_t* indices, const int32_t* offsets,
   // forward).
   P.credit_lag = h->credit_lag_opt >= 0 ? (int)h->credit_lag_opt : (h->shared_gpu ? 1 : 0);
   P.flat_below = (int)h->flat_below;
+  P.l1rows = h->l1_cur;
   P.skip_to = (int)h->skip_to;
   P.parity = (int)(h->epoch & 1);
   stage_layout(P, (int)h->stage_kb, (int)h->idx_cap);
@@ -1477,6 +1486,9 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
   } else if (k == "idx_cap") {
     if (v < 0 || v > 16384) return fail(h, EMB_A2A_EINVAL, "idx_cap in [0, 16384]");
     h->idx_cap = v;
+  } else if (k == "l1_rows") {
+    if (v < -1 || v > 1) return fail(h, EMB_A2A_EINVAL, "l1_rows in {-1 (auto), 0, 1}");
+    h->l1_opt = v;                     // applied by the next forward's ensure_chunk
   } else if (k == "flat_below") {
     if (v < 0 || v > 1 << 20) return fail(h, EMB_A2A_EINVAL, "flat_below >= 0");
     h->flat_below = v;
@@ -1560,6 +1572,8 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "vec") *v = h->vec;
   else if (k == "pdl") *v = h->pdl;
   else if (k == "flat_below") *v = h->flat_below;
+  else if (k == "l1_rows") *v = h->l1_opt;
+  else if (k == "l1_rows_active") *v = h->l1_cur;
   else if (k == "stage_kb") *v = h->stage_kb;
   else if (k == "ctas_per_sm") *v = h->ctas_per_sm;
   else if (k == "pdl_rows_early") *v = h->rows_early;

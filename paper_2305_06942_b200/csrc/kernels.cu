@@ -114,7 +114,9 @@ cudaError_t plan_with(const void* fn, const KParams& P, const LaunchCfg& c, Laun
 static cudaError_t plan_any(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl) {
   const bool weighted = P.weights != nullptr;
   switch (P.elem) {
-    case 0: return weighted ? plan_f32w(P, c, fused, pl) : plan_f32(P, c, fused, pl);
+    case 0:
+      if (weighted) return plan_f32w(P, c, fused, pl);
+      return (P.l1rows && !P.tma) ? plan_f32l1(P, c, fused, pl) : plan_f32(P, c, fused, pl);
     case 1: return plan_bf16(P, c, fused, weighted, pl);
     case 2: return plan_f16(P, c, fused, weighted, pl);
     default: return cudaErrorInvalidValue;

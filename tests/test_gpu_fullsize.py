@@ -40,17 +40,20 @@ def _tables(cfg, r, dtype):
     return out
 
 
-def _sampled_parity(name, W, dtype=torch.float32, value_mode=0, nsample=96):
+def _sampled_parity(name, W, dtype=torch.float32, value_mode=0, nsample=96, opts=None,
+                    l1_active=None):
     from paper_2305_06942_b200 import LoopbackGroup
     cfg = synth.config_for(name, W=W, value_mode=value_mode)
     csr = synth.gen_all_csr(cfg, 0)
-    grp = LoopbackGroup(W, dev())
+    grp = LoopbackGroup(W, dev(), opts)
     tabs = [_tables(cfg, r, dtype) for r in range(W)]
     grp.register_tables(tabs, cfg.B)
     idx = [torch.from_numpy(c[0]).to(dev()) for c in csr]
     off = [torch.from_numpy(c[1]).to(dev()) for c in csr]
     outs = grp.forward(idx, off)
     outs = grp.forward(idx, off)        # the second half of the double buffer, same inputs
+    if l1_active is not None:
+        assert all(h.get_option("l1_rows_active") == l1_active for h in grp.handles)
     rng = np.random.default_rng(W)
     try:
         for s in range(W):
@@ -72,6 +75,17 @@ def _sampled_parity(name, W, dtype=torch.float32, value_mode=0, nsample=96):
                                     ("weak", 4), ("weak", 8)])
 def test_full_size_forward_sampled_rows(name, W):
     _sampled_parity(name, W)
+
+
+@pytest.mark.parametrize("name,l1,active", [("sweep_p8", -1, 1), ("dlrm_wide", -1, 1),
+                                           ("sweep_p1", -1, 1), ("dlrm_small", -1, 0),
+                                           ("weak", -1, 0), ("dlrm_small", 1, 1),
+                                           ("dlrm_wide", 0, 0)])
+def test_full_size_l1_rows_choice(name, l1, active):
+    """The auto L1 choice (rows allocated in L1 from 4096 lookups per SM or 4096 bags per table:
+    sweep and DLRM-wide yes, DLRM-small and weak at W=1 no) and both forced settings, at full
+    size, against the oracle."""
+    _sampled_parity(name, 1, opts={"l1_rows": l1}, l1_active=active)
 
 
 def test_full_size_dlrm_wide_bf16_tables():

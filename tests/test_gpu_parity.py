@@ -91,10 +91,12 @@ def test_random_configs_vs_oracle(seed):
     g.destroy()
 
 
-@pytest.mark.parametrize("tma,vec", [(0, 0), (1, 0), (0, 2), (0, 4), (0, 8)])
+@pytest.mark.parametrize("tma,vec,l1", [(0, 0, 0), (1, 0, 0), (0, 2, 0), (0, 4, 0), (0, 8, 0),
+                                         (0, 0, 1), (0, 4, 1)])
 @pytest.mark.parametrize("D", [4, 8, 12, 16, 60, 64, 92, 128, 132, 256, 384, 512, 1024])
-def test_all_lane_mappings(D, tma, vec):
-    """Every lane mapping (LPB 1..32, NV 1..8) incl. masked columns (D/4 not a power of 2)."""
+def test_all_lane_mappings(D, tma, vec, l1):
+    """Every lane mapping (LPB 1..32, NV 1..8) incl. masked columns (D/4 not a power of 2), with
+    rows streamed past L1 and allocated in L1 (the "l1_rows" instance set)."""
     rng = np.random.default_rng(D)
     W, T, B = 2, [2, 3], 24
     G = sum(T)
@@ -107,8 +109,9 @@ def test_all_lane_mappings(D, tma, vec):
         idx.append(i)
         off.append(o)
     p = Problem(W, T, D, B, synth.even_partition(B, W), tables, idx, off)
-    g = make_group(p, {"tma": tma, "vec": vec})
+    g = make_group(p, {"tma": tma, "vec": vec, "l1_rows": l1})
     check(g.forward(*dev_csr(p)), oracle_out(p), exact=True)
+    assert g.handles[0].get_option("l1_rows_active") == (1 if l1 else 0)
     g.destroy()
 
 
@@ -122,6 +125,9 @@ def test_all_lane_mappings(D, tma, vec):
     {"tma": 1, "stage_kb": 3}, {"tma": 1, "stages": 8, "stage_kb": 64}, {"chunk": 1}, {"chunk": 3}, {"chunk": 63},
     {"chunk": 32, "slice": 64}, {"vec": 2}, {"vec": 4}, {"vec": 8}, {"vec": 2, "chunk": 32}, {"pdl": 0}, {"flat_below": 0}, {"flat_below": 1000},
     {"flat_below": 1000, "vec": 2}, {"flat_below": 1000, "idx_cap": 4},
+    {"l1_rows": 1}, {"l1_rows": 1, "flat_below": 0}, {"l1_rows": 1, "flat_below": 1000},
+    {"l1_rows": 1, "vec": 4}, {"l1_rows": 1, "idx_cap": 0}, {"l1_rows": 1, "tma": 1},
+    {"l1_rows": 0},
 ])
 def test_results_invariant_to_tunables(opts):
     """Slice size, schedule, CTA size, unroll and index staging must not change any bit."""
