@@ -238,7 +238,7 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *   "flat_below"   pipeline stages whose average bag length is below this (default 12) pool with a
  *                  row-flattened loop (rows of several short bags in flight at once); longer
  *                  bags use the per-bag loop.  0 = always per-bag, large = always flattened
- *   "l1_rows"      fp32 unweighted tables, LSU gathers: -1 auto (default: when the forward has
+ *   "l1_rows"      unweighted forwards, LSU gathers: -1 auto (default: when the forward has
  *                  >= 4096 lookups per SM or B >= 4096 bags per table), 0 rows stream past L1
  *                  (L1::no_allocate), 1 rows are
  *                  allocated in L1 (a Zipf-hot row recurring on the same SM is served there).

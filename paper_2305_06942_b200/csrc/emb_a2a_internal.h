@@ -77,7 +77,7 @@ struct KParams {
                       // only by exiting)
   int credit_lag;     // a peer's credit must reach epoch - credit_lag before we store into it
   int flat_below;     // stages whose average bag length is below this use row-flattened pooling
-  int l1rows;         // fp32 unweighted LSU gathers: rows allocated in L1 (instance set ELEM 3)
+  int l1rows;         // unweighted LSU gathers: rows allocated in L1 (instance sets ELEM 3-5)
   long long part[kMaxW + 1];    // batch partition prefix
   int slice_base[kMaxW + 1];    // first slice of destination ordinal k; [W] = nslices
   int chunk_base[kMaxW + 1];    // first chunk of destination ordinal k; [W] = nchunks
@@ -162,6 +162,8 @@ cudaError_t plan_with(const void* fn, const KParams& P, const LaunchCfg& c, Laun
 cudaError_t plan_f32(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
 cudaError_t plan_f32w(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
 cudaError_t plan_f32l1(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
+cudaError_t plan_bf16l1(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
+cudaError_t plan_f16l1(const KParams& P, const LaunchCfg& c, bool fused, LaunchPlan* pl);
 cudaError_t plan_bf16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,
                       LaunchPlan* pl);
 cudaError_t plan_f16(const KParams& P, const LaunchCfg& c, bool fused, bool weighted,

@@ -151,9 +151,9 @@ __device__ __forceinline__ float lds_f32(unsigned addr) {
   return v;
 }
 
-// Table element types: 0 = fp32 (4 per 16-byte unit), 1 = bf16, 2 = fp16 (8 per unit); 3 = fp32
-// with L1-allocating row loads (ld_unit_pred).  Every element is converted EXACTLY to fp32 before
-// it is accumulated (R#28).
+// Table element types: 0 = fp32 (4 per 16-byte unit), 1 = bf16, 2 = fp16 (8 per unit); 3, 4, 5 =
+// fp32, bf16, fp16 with L1-allocating row loads (ld_unit_pred).  Every element is converted
+// EXACTLY to fp32 before it is accumulated (R#28).
 template <int ELEM>
 struct Elem {
   static constexpr int EPU = (ELEM == 0 || ELEM == 3) ? 4 : 8;
@@ -164,7 +164,7 @@ __device__ __forceinline__ void unit_to_f(const uint4& u, float (&f)[Elem<ELEM>:
   if constexpr (ELEM == 0 || ELEM == 3) {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
     f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
-  } else if constexpr (ELEM == 1) {   // bf16 = top half of binary32
+  } else if constexpr (ELEM == 1 || ELEM == 4) {   // bf16 = top half of binary32
     const unsigned w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -290,7 +290,7 @@ __device__ __forceinline__ void pool_bag_lsu(const uint4* __restrict__ tab, int 
     for (int u = 0; u < U; ++u) {
       const uint4* r = tab + (size_t)(unsigned)row[u] * DU + lane;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<ELEM == 3>(r + v * LPB, colok[v] && (u < n));
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<(ELEM >= 3)>(r + v * LPB, colok[v] && (u < n));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -377,7 +377,7 @@ __device__ __forceinline__ void pool_run_lsu(const uint4* __restrict__ tab, int 
     for (int u = 0; u < U; ++u) {
       const uint4* r = tab + (size_t)(unsigned)row[u] * DU + lane;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<ELEM == 3>(r + v * LPB, colok[v] && (u < n));
+      for (int v = 0; v < NV; ++v) x[u][v] = ld_unit_pred<(ELEM >= 3)>(r + v * LPB, colok[v] && (u < n));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -117,8 +117,12 @@ static cudaError_t plan_any(const KParams& P, const LaunchCfg& c, bool fused, La
     case 0:
       if (weighted) return plan_f32w(P, c, fused, pl);
       return (P.l1rows && !P.tma) ? plan_f32l1(P, c, fused, pl) : plan_f32(P, c, fused, pl);
-    case 1: return plan_bf16(P, c, fused, weighted, pl);
-    case 2: return plan_f16(P, c, fused, weighted, pl);
+    case 1:
+      return (P.l1rows && !weighted) ? plan_bf16l1(P, c, fused, pl)
+                                     : plan_bf16(P, c, fused, weighted, pl);
+    case 2:
+      return (P.l1rows && !weighted) ? plan_f16l1(P, c, fused, pl)
+                                     : plan_f16(P, c, fused, weighted, pl);
     default: return cudaErrorInvalidValue;
   }
 }

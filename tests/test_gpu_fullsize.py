@@ -88,6 +88,9 @@ def test_full_size_l1_rows_choice(name, l1, active):
     _sampled_parity(name, 1, opts={"l1_rows": l1}, l1_active=active)
 
 
-def test_full_size_dlrm_wide_bf16_tables():
-    """DLRM-wide with bf16 tables (value mode 2: k * 2^-7, exact in bf16), fp32 accumulation."""
-    _sampled_parity("dlrm_wide", 1, dtype=torch.bfloat16, value_mode=2)
+@pytest.mark.parametrize("l1", [-1, 0])
+def test_full_size_dlrm_wide_bf16_tables(l1):
+    """DLRM-wide with bf16 tables (value mode 2: k * 2^-7, exact in bf16), fp32 accumulation;
+    rows through L1 (auto at DLRM-wide) and streamed."""
+    _sampled_parity("dlrm_wide", 1, dtype=torch.bfloat16, value_mode=2, opts={"l1_rows": l1},
+                    l1_active=1 if l1 else 0)

@@ -75,7 +75,8 @@ def test_half_lane_mappings(dtype, D):
         off.append(o)
     p = Problem(W, T, D, B, synth.even_partition(B, W), bits, idx, off)
     ref = oracle.emb_a2a(p.part, D, B, T, bits, idx, off, dtype=dtype)
-    for opts in ({}, {"vec": 2}, {"vec": 4}):
+    for opts in ({}, {"vec": 2}, {"vec": 4}, {"l1_rows": 1}, {"l1_rows": 1, "vec": 4},
+                 {"l1_rows": 1, "flat_below": 1000}):
         got = run_gpu(p, [to_dev_table(b, dtype) for b in bits], opts=opts, dtype=DT[dtype])
         for a, b in zip(got, ref):
             np.testing.assert_array_equal(a, b)
