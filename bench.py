@@ -663,7 +663,8 @@ def main():
                    "parallelism": f"table-wise MP x{N} -> batch DP x{N}",
                    "slice": h.get_option("slice"), "threads": h.get_option("threads"),
                    "order": h.get_option("order"), "ctas_per_sm": h.get_option("ctas_per_sm"),
-                   "chunk_bags": h.query("chunk_bags"), "opts": list(args.opt),
+                   "chunk_bags": h.query("chunk_bags"),
+                   "l1_rows": h.get_option("l1_rows_active"), "opts": list(args.opt),
                    "skew_us_last_rank": args.skew_us,
                    "l2": ("inputs larger than L2: %d rotating batches (~%.0f MB of indices + "
                           "distinct rows) over %.1f GB of tables, K back-to-back steps" %
