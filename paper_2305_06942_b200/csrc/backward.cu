@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(256) bwd_keygen_kernel(const SortParams S) {
           S.bags[p] = (int)bag;
           if (WEIGHTED) S.wts[p] = wv[u];
           for (int q = 0; q < S.passes; ++q)   // the last digit may be narrower
-            atomicAdd(&h[q * 256 + ((key >> (8 * q)) & (q == S.passes - 1 ? S.last_mask : 255u))],
+            atomicAdd(&h[q * 256 + ((key >> (S.hshift + 8 * q)) &
+                                    (q == S.passes - 1 ? S.last_mask : 255u))],
                       1u);
         }
       }
@@ -831,6 +832,188 @@ __global__ void __launch_bounds__(kSortThreads) bwd_onesweep_seg_kernel(const Pa
   }
 }
 
+// Exclusive scan of one value per thread over a block of NW warps.
+template <int NW>
+__device__ __forceinline__ unsigned block_excl_scan_nw(unsigned v, unsigned* s_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  unsigned base = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) base += i < w ? s_warp[i] : 0u;
+  __syncthreads();                     // s_warp may be reused right after
+  return base + x - v;
+}
+
+// ------------------------------------------------------------------- bucket sort plan
+// sort_mode 5: keygen (histogram of the TOP 8 key bits only), one stable onesweep pass on that
+// top digit -- 256 buckets, each a contiguous, position-ordered range -- then ONE kernel sorts
+// every bucket on its own by the remaining low bits (stable LSD passes of 8 bits), one CTA per
+// bucket, entirely in shared memory: no cross-CTA coordination after the first pass, so the
+// look-back chains and kernel boundaries of passes 2.. disappear.  A bucket larger than the
+// shared-memory capacity is sorted the same way in global memory (the plan's ping-pong buffers).
+// Same stable order as the plain plan: MSD on the top digit, then LSD within each bucket.
+struct BucketParams {
+  const unsigned* keys_in;     // after the top-digit pass (buffer 1)
+  const int* bags_in;
+  const float* wts_in;
+  unsigned* keys_out;          // the plan's output (buffer 0)
+  int* bags_out;
+  float* wts_out;
+  const unsigned* hist;        // [256] top-digit counts (keygen)
+  int low_bits;                // key bits below the top digit
+  int cap;                     // keys a bucket may have to sort in shared memory
+};
+
+// 256 threads x 8 keys per tile (measured r02at/r02au: 1024 threads x 4 only moved DLRM-small's
+// bucket kernel 30.4 -> 27.4 us and slowed sweep P=1's plan 32.5 -> 38.7 us)
+constexpr int kBktThreads = 256;
+constexpr int kBktItems = 8;
+template <bool WEIGHTS>
+__global__ void __launch_bounds__(kBktThreads, 1) bwd_bucket_sort_kernel(const BucketParams P) {
+  constexpr int NT = kBktThreads, NW = NT / 32, K = kBktItems, TILE = NT * K;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned s_base[256], s_run[256], s_tot[256], s_warp[NW];
+  __shared__ unsigned short s_cnt[NW][256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_wait();     // the top-digit pass is complete
+  pdl_trigger();
+  const unsigned hv = tid < 256 ? P.hist[tid] : 0u;
+  const unsigned start = block_excl_scan_nw<NW>(hv, s_warp);
+  if (tid == blockIdx.x) s_base[0] = start;            // (s_base reused below)
+  __syncthreads();
+  const unsigned b0 = s_base[0];
+  const int nb = (int)P.hist[blockIdx.x];
+  if (nb == 0) return;
+  const int passes = (P.low_bits + 7) / 8;
+  const bool in_smem = nb <= P.cap;
+  // ping-pong: shared memory (two arrays of cap) or the plan's global buffers
+  unsigned* sk[2];
+  int* sb[2];
+  float* sw[2];
+  sk[0] = reinterpret_cast<unsigned*>(smem);
+  sb[0] = reinterpret_cast<int*>(sk[0] + P.cap);
+  sw[0] = reinterpret_cast<float*>(sb[0] + P.cap);
+  sk[1] = reinterpret_cast<unsigned*>(sw[0] + (WEIGHTS ? P.cap : 0));
+  sb[1] = reinterpret_cast<int*>(sk[1] + P.cap);
+  sw[1] = reinterpret_cast<float*>(sb[1] + P.cap);
+  unsigned* gk[2] = {const_cast<unsigned*>(P.keys_in) + b0, P.keys_out + b0};
+  int* gb[2] = {const_cast<int*>(P.bags_in) + b0, P.bags_out + b0};
+  float* gw[2] = {WEIGHTS ? const_cast<float*>(P.wts_in) + b0 : nullptr,
+                  WEIGHTS ? P.wts_out + b0 : nullptr};
+  int cur = 0;                                  // index of the array holding the current order
+  if (in_smem) {
+    for (int i = tid; i < nb; i += NT) {
+      sk[0][i] = __ldcg(gk[0] + i);
+      sb[0][i] = __ldcg(gb[0] + i);
+      if (WEIGHTS) sw[0][i] = __ldcg(gw[0] + i);
+    }
+    __syncthreads();
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    const unsigned dmask = (1u << min(8, P.low_bits - shift)) - 1u;
+    // (selects, not runtime indexing: keeps the pointers in registers)
+    unsigned* const kin = in_smem ? (cur ? sk[1] : sk[0]) : (cur ? gk[1] : gk[0]);
+    int* const bin = in_smem ? (cur ? sb[1] : sb[0]) : (cur ? gb[1] : gb[0]);
+    float* const win = in_smem ? (cur ? sw[1] : sw[0]) : (cur ? gw[1] : gw[0]);
+    unsigned* const kout = in_smem ? (cur ? sk[0] : sk[1]) : (cur ? gk[0] : gk[1]);
+    int* const bout = in_smem ? (cur ? sb[0] : sb[1]) : (cur ? gb[0] : gb[1]);
+    float* const wout = in_smem ? (cur ? sw[0] : sw[1]) : (cur ? gw[0] : gw[1]);
+    // the bucket's digit counts -> exclusive base per digit
+    if (tid < 256) s_tot[tid] = 0u;
+    __syncthreads();
+    for (int i = tid; i < nb; i += NT) {
+      const unsigned k = in_smem ? kin[i] : __ldcg(kin + i);
+      atomicAdd(&s_tot[(k >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    {
+      const unsigned ex = block_excl_scan_nw<NW>(tid < 256 ? s_tot[tid] : 0u, s_warp);
+      if (tid < 256) s_run[tid] = ex;
+    }
+    __syncthreads();
+    for (int base = 0; base < nb; base += TILE) {
+      unsigned key[K], dg[K];
+      int bag[K];
+      float wt[K];
+      unsigned short rank[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int pos = base + w * (32 * K) + i * 32 + lane;
+        const bool valid = pos < nb;
+        key[i] = valid ? (in_smem ? kin[pos] : __ldcg(kin + pos)) : 0u;
+        bag[i] = valid ? (in_smem ? bin[pos] : __ldcg(bin + pos)) : 0;
+        if (WEIGHTS) wt[i] = valid ? (in_smem ? win[pos] : __ldcg(win + pos)) : 0.f;
+        dg[i] = valid ? ((key[i] >> shift) & dmask) : 256u;
+      }
+      for (int i = tid; i < NW * 256 / 2; i += NT)
+        reinterpret_cast<unsigned*>(&s_cnt[0][0])[i] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const unsigned peers = __match_any_sync(kFull, dg[i]);
+        const unsigned c = dg[i] < 256u ? s_cnt[w][dg[i]] : 0u;
+        rank[i] = (unsigned short)(c + __popc(peers & lt_mask));
+        __syncwarp();
+        if (dg[i] < 256u && lane == __ffs(peers) - 1)
+          s_cnt[w][dg[i]] = (unsigned short)(c + __popc(peers));
+        __syncwarp();
+      }
+      __syncthreads();
+      if (tid < 256) {
+        unsigned acc = 0;
+#pragma unroll 8
+        for (int ww = 0; ww < NW; ++ww) {
+          const unsigned x = s_cnt[ww][tid];
+          s_cnt[ww][tid] = (unsigned short)acc;
+          acc += x;
+        }
+        s_tot[tid] = acc;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (dg[i] >= 256u) continue;
+        const unsigned o = s_run[dg[i]] + s_cnt[w][dg[i]] + rank[i];
+        kout[o] = key[i];
+        bout[o] = bag[i];
+        if (WEIGHTS) wout[o] = wt[i];
+      }
+      __syncthreads();
+      if (tid < 256) s_run[tid] += s_tot[tid];
+      __syncthreads();
+    }
+    cur ^= 1;
+    if (!in_smem) __threadfence_block();
+    __syncthreads();
+  }
+  // the result into the plan's output buffer (global index 1 = keys_out)
+  if (in_smem) {
+    const unsigned* const fk = cur ? sk[1] : sk[0];
+    const int* const fb = cur ? sb[1] : sb[0];
+    const float* const fw = cur ? sw[1] : sw[0];
+    for (int i = tid; i < nb; i += NT) {
+      gk[1][i] = fk[i];
+      gb[1][i] = fb[i];
+      if (WEIGHTS) gw[1][i] = fw[i];
+    }
+  } else if (cur == 0) {              // global ping-pong ended in the input buffer: copy over
+    for (int i = tid; i < nb; i += NT) {
+      gk[1][i] = __ldcg(gk[0] + i);
+      gb[1][i] = __ldcg(gb[0] + i);
+      if (WEIGHTS) gw[1][i] = __ldcg(gw[0] + i);
+    }
+  }
+}
+
 // ------------------------------------------------------------------- cluster sort plan
 // sort_mode 4: the whole plan in ONE kernel, one thread-block cluster of C CTAs per table.  The
 // input is table-major and the sort stable, so each table's segment is sorted by its row bits
@@ -878,24 +1061,6 @@ __device__ __forceinline__ void ld_dsmem(unsigned addr, unsigned rank, unsigned 
   }
 }
 
-// Exclusive scan of one value per thread over a block of NW warps.
-template <int NW>
-__device__ __forceinline__ unsigned block_excl_scan_nw(unsigned v, unsigned* s_warp) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_warp[w] = x;
-  __syncthreads();
-  unsigned base = 0;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) base += i < w ? s_warp[i] : 0u;
-  __syncthreads();                     // s_warp may be reused right after
-  return base + x - v;
-}
 
 // Per-CTA timeline of the cluster plan (the "trace" option): events 40 start, 41 keys generated,
 // then per pass (payload = pass) 43 the pass's counts complete (cluster barrier), 44 offsets
@@ -1872,6 +2037,30 @@ cudaError_t launch_sort_plan_seg(const SortParams& S, const PassParams* passes, 
   return cudaSuccess;
 }
 
+
+
+cudaError_t launch_bucket_sort(const unsigned* keys_in, const int* bags_in, const float* wts_in,
+                               unsigned* keys_out, int* bags_out, float* wts_out,
+                               const unsigned* hist, int low_bits, int cap, cudaStream_t st) {
+  BucketParams P;
+  P.keys_in = keys_in;
+  P.bags_in = bags_in;
+  P.wts_in = wts_in;
+  P.keys_out = keys_out;
+  P.bags_out = bags_out;
+  P.wts_out = wts_out;
+  P.hist = hist;
+  P.low_bits = low_bits;
+  P.cap = cap;
+  const bool w = wts_in != nullptr;
+  const void* fn = w ? reinterpret_cast<const void*>(bwd_bucket_sort_kernel<true>)
+                     : reinterpret_cast<const void*>(bwd_bucket_sort_kernel<false>);
+  const size_t sm = (size_t)2 * cap * (w ? 12 : 8);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&P};
+  return launch_pdl(fn, 256, kBktThreads, sm, st, args);
+}
 
 int cluster_plan_size(int T, int db, bool weights) {
   const void* fn = pick_cluster_fn(db, weights);

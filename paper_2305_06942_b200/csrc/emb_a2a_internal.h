@@ -204,6 +204,7 @@ struct SortParams {
   long long TB, B;
   int rbits, passes;
   unsigned last_mask;          // digit mask of the last pass (the key may end inside a digit)
+  int hshift;                  // bit of pass 0's digit (0; the bucket plan counts the TOP digit)
   unsigned* lbg;               // onesweep group look-back words of every pass (zeroed by keygen)
   long long lbg_words;
   // segmented plan (seg_db > 0): digits are row bits only, counted per (table, digit); the
@@ -265,6 +266,11 @@ struct ClusterSortParams {
   long long trace_cap;
 };
 cudaError_t launch_sort_plan_cluster(const ClusterSortParams& S, int T, cudaStream_t st);
+// Bucket plan (sort_mode 5): after keygen + one onesweep pass on the top 8 key bits, one CTA per
+// bucket sorts it by the low bits in shared memory (global memory above `cap` keys).
+cudaError_t launch_bucket_sort(const unsigned* keys_in, const int* bags_in, const float* wts_in,
+                               unsigned* keys_out, int* bags_out, float* wts_out,
+                               const unsigned* hist, int low_bits, int cap, cudaStream_t st);
 // CTAs per cluster the cluster plan would use for T tables (0 = cannot launch)
 int cluster_plan_size(int T, int db, bool weights);
 

@@ -141,6 +141,7 @@ struct emb_a2a {
 
   // backward (f3)
   int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0, sort_stall = 0;
+  int64_t bucket_cap = 8192;             // bucket plan: keys a bucket sorts in shared memory
   int64_t cluster_ctas = 0;              // cluster plan: CTAs per table (0 auto)
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
@@ -1156,7 +1157,13 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   // words), so 2 wide passes only tie 3-4 narrow ones; auto keeps the plain plan (option 3 only).
   const bool seg = h->T >= 1 && h->T <= 256 && rbits <= 22 && h->sort_mode == 3;
   (void)sms0;
-  const int passes = seg ? 2 : (kbits + 7) / 8;
+  // bucket plan (sort_mode 5): one pass on the top 8 key bits, then per-bucket local sorts
+  // (auto for large plans of small buckets -- <= 1024 keys per bucket on average: measured r02as,
+  // sweep P=1 plan 49.7 -> 32.5 us; DLRM-small, 1280 per bucket but a 5 K-key Zipf-hot bucket,
+  // 39.8 -> 43.2 us, so the plain plan stays the default there)
+  const bool bkt = kbits > 8 && (h->sort_mode == 5 ||
+                                 (h->sort_mode == 0 && n >= (1 << 16) && n <= 256 * 1024));
+  const int passes = seg ? 2 : bkt ? 1 : (kbits + 7) / 8;
   const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const bool wtd = weights != nullptr && n > 0;
@@ -1270,7 +1277,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   h->plan_weighted = wtd;
   h->plan_offsets = offsets;
   h->plan_n = n;
-  h->plan_buf = passes & 1;
+  h->plan_buf = bkt ? 0 : passes & 1;   // the bucket sort writes buffer 0
   h->planned = true;
   if (n == 0) return EMB_A2A_OK;
   // this plan's digit counts and tile tickets: the half zeroed by the previous plan's keygen (or
@@ -1290,7 +1297,8 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   S.B = h->B;
   S.rbits = rbits;
   S.passes = passes;
-  S.last_mask = passes > 0 ? (1u << (kbits - 8 * (passes - 1))) - 1u : 0u;
+  S.last_mask = bkt ? 255u : passes > 0 ? (1u << (kbits - 8 * (passes - 1))) - 1u : 0u;
+  S.hshift = bkt ? kbits - 8 : 0;
   S.lbg = h->d_lbg;
   S.lbg_words = (long long)nlbg;
   PassParams pp[kMaxPasses];
@@ -1311,7 +1319,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
     q.gsum = q.garrive + ngroups;
     q.ntiles = ntiles;
     q.n = n;
-    q.shift = 8 * p;
+    q.shift = bkt ? kbits - 8 : 8 * p;
     q.dmask = p == passes - 1 ? S.last_mask : 255u;
     q.stamp = h->plan_no;
     q.trace = h->d_trace;
@@ -1352,7 +1360,11 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   cudaError_t e = seg ? launch_sort_plan_seg(S, pp, passes, ntiles_seg,
                                              (int)std::max<long long>(gk, 1), st)
                       : launch_sort_plan(S, pp, passes, ntiles, (int)std::max<long long>(gk, 1),
-                                         (int)h->sort_mode, st);
+                                         bkt ? 1 : (int)h->sort_mode, st);
+  if (e == cudaSuccess && bkt)
+    e = launch_bucket_sort(h->d_keys[1], h->d_bags[1], wtd ? h->d_wts[1] : nullptr, h->d_keys[0],
+                           h->d_bags[0], wtd ? h->d_wts[0] : nullptr, hb, kbits - 8,
+                           (int)h->bucket_cap, st);
   if (e != cudaSuccess) {
     h->planned = false;
     cudaMemsetAsync(h->d_hist, 0, 2 * kHistWords * sizeof(unsigned), st);   // both halves clean
@@ -1361,7 +1373,7 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   }
   if (n > 0) h->last_seg = seg ? 1 : 0;
   h->hist_par ^= 1;
-  h->kernel_launches += 1 + passes;
+  h->kernel_launches += 1 + passes + (bkt ? 1 : 0);
   return EMB_A2A_OK;
 }
 
@@ -1528,8 +1540,12 @@ int emb_a2a_set_option(emb_a2a_t* h, const char* key, int64_t v) {
     if (v < -1 || v > 1) return fail(h, EMB_A2A_EINVAL, "debug_credit_lag in {-1, 0, 1}");
     h->credit_lag_opt = v;
   } else if (k == "sort_mode") {
-    if (v < 0 || v > 4) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3, 4}");
+    if (v < 0 || v > 5) return fail(h, EMB_A2A_EINVAL, "sort_mode in {0, 1, 2, 3, 4, 5}");
     h->sort_mode = v;
+  } else if (k == "bucket_cap") {
+    if (v < 256 || v > 8192 || v % 256)
+      return fail(h, EMB_A2A_EINVAL, "bucket_cap: 256..8192, multiple of 256");
+    h->bucket_cap = v;
   } else if (k == "cluster_ctas") {
     if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16)
       return fail(h, EMB_A2A_EINVAL, "cluster_ctas in {0 (auto), 1, 2, 4, 8, 16}");
@@ -1580,6 +1596,7 @@ int emb_a2a_get_option(const emb_a2a_t* h, const char* key, int64_t* v) {
   else if (k == "debug_credit_lag") *v = h->credit_lag_opt;
   else if (k == "sort_mode") *v = h->sort_mode;
   else if (k == "cluster_ctas") *v = h->cluster_ctas;
+  else if (k == "bucket_cap") *v = h->bucket_cap;
   else if (k == "bwd_threads") *v = h->bwd_threads;
   else if (k == "bwd_share") *v = h->bwd_share;
   else if (k == "debug_delay_ns") *v = h->delay_ns;

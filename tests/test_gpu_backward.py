@@ -454,7 +454,7 @@ def test_plans_in_any_sequence_use_clean_buffers():
     h.destroy()
 
 
-@pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p8", "dlrm_wide"])
+@pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p1", "sweep_p8", "dlrm_wide"])
 def test_full_size_backward_sampled_rows(name):
     """BASELINE config at full size (W=1 per-rank work, as bench.py times it): the plan sorts
     every lookup; check the updated table on sampled rows against the oracle on just the
@@ -707,6 +707,119 @@ def test_cluster_plan_full_size_equals_plain(name):
     from paper_2305_06942_b200 import EmbA2A, LocalGroup
     outs = []
     for mode in (0, 4):
+        h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0), {"sort_mode": mode})
+        tabs = [torch.zeros(cfg.R, cfg.D, device=dev()) for _ in range(cfg.T[0])]
+        h.register_tables(tabs, cfg.B)
+        h.backward_plan(idx, off)
+        h.backward(grad, -1.0)
+        torch.cuda.synchronize()
+        h.check()
+        outs.append(tabs)
+        h.destroy()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    del outs
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------- bucket plan (sort_mode 5)
+
+@pytest.mark.parametrize("cap", [8192, 256])
+@pytest.mark.parametrize("seed,W,weighted", [(0, 1, False), (1, 1, True), (2, 2, False),
+                                             (3, 4, False), (4, 2, True)])
+def test_bucket_plan_exact_vs_oracle(seed, W, weighted, cap):
+    """The bucket plan (sort_mode 5: a pass on the top key digit, then every bucket sorted by
+    its low bits in shared memory, or in global memory above bucket_cap) gives the oracle's
+    tables bitwise in exact-int mode."""
+    p, w = _seg_problem(7400 + seed, W, weighted)
+    grads = grads_for(p, seed, 1)
+    kw = {} if w is None else {"weights": w}
+    want = oracle.backward_sgd(p.part, p.D, p.B, p.T, p.tables, p.indices, p.offsets, grads, 0.5, **kw)
+    run = Run(p, opts={"sort_mode": 5, "bucket_cap": cap})
+    run.backward(grads, 0.5, weights=w)
+    for a, b in zip(run.tables(), want):
+        np.testing.assert_array_equal(a, b)
+    run.destroy()
+
+
+@pytest.mark.parametrize("cap", [8192, 512])
+@pytest.mark.parametrize("seed,W,weighted,rows", [(0, 1, False, (1 << 16, 1 << 18)),
+                                                  (1, 1, True, (1 << 18, 1 << 20)),
+                                                  (2, 2, False, (1 << 20, 1 << 22)),
+                                                  (4, 1, False, (1 << 8, 1 << 9)),
+                                                  (5, 1, True, (40, 200))])
+def test_bucket_plan_equals_plain_plan(seed, W, weighted, rows, cap):
+    """Key widths from 8 to 24 bits (0 to 3 local passes per bucket): the bucket plan's order is
+    the plain plan's, so the updated tables are bitwise those of sort_mode 1 (fp32 values)."""
+    p, w = _seg_problem(7450 + seed, W, weighted, rows)
+    grads = grads_for(p, seed, 0)
+    outs = []
+    for mode, opts in ((1, {}), (5, {"bucket_cap": cap})):
+        run = Run(p, opts=dict(opts, sort_mode=mode))
+        run.backward(grads, 0.5, weights=w)
+        outs.append(run.tables())
+        run.destroy()
+    for a, b in zip(outs[1], outs[0]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", ["one_row", "tiny_batch", "empty_bags", "one_table", "mean",
+                                  "hot_row"])
+def test_bucket_plan_degenerate(case):
+    """Edge cases of the bucket plan vs the oracle (exact-int): every row 0 (a key of the table
+    bits only), 3 bags, mostly empty bags, one table, mean pooling, and one row looked up by
+    every bag (a bucket above the shared-memory capacity: the global-memory path)."""
+    rng = np.random.default_rng(78)
+    D, T, R, B, maxL = 8, 3, 500, 256, 12
+    pooling = "sum"
+    if case == "one_row":
+        R = 1
+    elif case == "tiny_batch":
+        B = 3
+    elif case == "empty_bags":
+        maxL = 1
+    elif case == "one_table":
+        T = 1
+    elif case == "mean":
+        pooling = "mean"
+    tables = [rng.integers(-8, 8, (R, D)).astype(np.float32) for _ in range(T)]
+    if case == "hot_row":
+        B = 2048
+        bags = [[[5] * int(rng.integers(2, 8)) + list(rng.integers(0, R, 2)) for _ in range(B)]
+                for _ in range(T)]
+    else:
+        bags = [[list(rng.integers(0, R, rng.integers(0, maxL + 1))) for _ in range(B)]
+                for _ in range(T)]
+    i, o = csr_from_bags(bags)
+    p = Problem(1, [T], D, B, np.array([0, B]), tables, [i], [o])
+    grads = grads_for(p, 3, 1)
+    kw = {"pooling": oracle.MEAN} if pooling == "mean" else {}
+    want = oracle.backward_sgd(p.part, D, B, p.T, p.tables, p.indices, p.offsets, grads, 0.5, **kw)
+    run = Run(p, pooling=pooling, opts={"sort_mode": 5, "bucket_cap": 1024})
+    run.backward(grads, 0.5)
+    got = run.tables()
+    run.destroy()
+    if pooling == "mean":
+        bound_check(p, got, want, grads, 0.5, pooling=oracle.MEAN)
+    else:
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p1", "sweep_p8", "dlrm_wide"])
+def test_bucket_plan_full_size_equals_plain(name):
+    """BASELINE configs at full size: the bucket plan's tables are bitwise those of the plain
+    plan (fp32 gradients: equal results need the same lookup order); sweep P=1 takes the bucket
+    plan by default (auto), the others are forced."""
+    cfg = synth.config_for(name, W=1)
+    idx_h, off_h = synth.gen_all_csr(cfg, 0)[0]
+    rng = np.random.default_rng(1)
+    grad = torch.from_numpy(rng.standard_normal((cfg.B, cfg.G * cfg.D)).astype(np.float32)).to(dev())
+    idx = torch.from_numpy(idx_h).to(dev())
+    off = torch.from_numpy(off_h).to(dev())
+    from paper_2305_06942_b200 import EmbA2A, LocalGroup
+    outs = []
+    for mode in (1, 5):
         h = EmbA2A(0, 1, dev(), LocalGroup(1).allgather_for(0), {"sort_mode": mode})
         tabs = [torch.zeros(cfg.R, cfg.D, device=dev()) for _ in range(cfg.T[0])]
         h.register_tables(tabs, cfg.B)
