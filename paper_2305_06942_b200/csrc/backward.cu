@@ -19,6 +19,10 @@
 //                        the same pass as reduce-then-scan: tile digit counts, a per-digit scan
 //                        over tiles, then warp-level ranking with match.any and a digit-ordered,
 //                        contiguous write-out of each tile (more tiles than one wave)
+//   bwd_bucket_sort_kernel  (bucket plan) after a onesweep pass on the top key digit, one CTA
+//                        per bucket sorts it by the low bits in shared memory
+//   bwd_cluster_sort_kernel (cluster plan, option) keygen + every row-digit pass of a table in
+//                        one thread-block cluster, digit counts exchanged through DSMEM
 //   bwd_kernel           pass 1 (fused) each CTA first pushes its share of this rank's gradient
 //                        rows straight into the owners' staging buffers over NVLink (zero-copy,
 //                        the reverse of P:165; a store into owner q waits for q's credit) and
