@@ -277,7 +277,8 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *   "trace"        N > 0: record up to N per-CTA %globaltimer events per forward (the paper's
  *                  per-WG timeline); 0 = off (default).  Read with emb_a2a_read_trace.
  *   "sort_mode"    backward plan's radix passes: 0 auto (default: the bucket plan (5) for
- *                  65536..262144 lookups, else one kernel per 8-bit pass with look-back while the
+ *                  65536..524288 lookups with <= 32768 per table, else one kernel per 8-bit
+ *                  pass with look-back while the
  *                  tiles fit one wave, else three kernels per pass, reduce-then-scan), 1 always
  *                  one kernel, 2 always three, 3 the segmented plan
  *                  (each table's lookups sorted by row bits only: 2 passes of <= 11-bit digits,
@@ -288,7 +289,8 @@ int emb_a2a_peer_store_probe(emb_a2a_t* h, int64_t bytes_per_peer, void* stream,
  *                  the bucket plan (one pass on the top 8 key bits, then one CTA per bucket sorts
  *                  it by the low bits in shared memory) -- results identical in every mode
  *   "bucket_cap"   bucket plan: keys a bucket may hold to be sorted in shared memory (default
- *                  8192; multiple of 256 in 256..8192); larger buckets sort in global memory
+ *                  4096; multiple of 256 in 256..8192; shared memory per CTA = 16 B x cap, so
+ *                  larger caps fit fewer CTAs per SM); larger buckets sort in global memory
  *   "cluster_ctas" cluster plan: CTAs per table cluster, 0 auto (default: the largest of 16, 8,
  *                  4, 2 whose T clusters fit two CTAs per SM, else 1; smaller if the occupancy
  *                  query says a cluster cannot be resident), or 1, 2, 4, 8, 16

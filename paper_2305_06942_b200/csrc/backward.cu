@@ -934,9 +934,20 @@ __global__ void __launch_bounds__(kBktThreads, 1) bwd_bucket_sort_kernel(const B
     // the bucket's digit counts -> exclusive base per digit
     if (tid < 256) s_tot[tid] = 0u;
     __syncthreads();
-    for (int i = tid; i < nb; i += NT) {
-      const unsigned k = in_smem ? kin[i] : __ldcg(kin + i);
-      atomicAdd(&s_tot[(k >> shift) & dmask], 1u);
+    {
+      // 8 keys per thread in flight (global path: one round trip per 8 x NT keys)
+      constexpr int LB = 8;
+      for (int i0 = 0; i0 < nb; i0 += LB * NT) {
+        unsigned kk[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int i = i0 + u * NT + tid;
+          kk[u] = i < nb ? (in_smem ? kin[i] : __ldcg(kin + i)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u)
+          if (i0 + u * NT + tid < nb) atomicAdd(&s_tot[(kk[u] >> shift) & dmask], 1u);
+      }
     }
     __syncthreads();
     {

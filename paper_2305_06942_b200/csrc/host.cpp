@@ -141,7 +141,7 @@ struct emb_a2a {
 
   // backward (f3)
   int64_t bwd_threads = 128, bwd_share = 1, sort_mode = 0, sort_stall = 0;
-  int64_t bucket_cap = 8192;             // bucket plan: keys a bucket sorts in shared memory
+  int64_t bucket_cap = 4096;             // bucket plan: keys a bucket sorts in shared memory
   int64_t cluster_ctas = 0;              // cluster plan: CTAs per table (0 auto)
   uint64_t bepoch = 0;                   // fused backwards issued (exchange epochs, parity)
   uint32_t plan_no = 0;                  // sort plans (look-back stamps)
@@ -1158,11 +1158,14 @@ int emb_a2a_backward_plan(emb_a2a_t* h, const int32_t* indices, const int32_t* o
   const bool seg = h->T >= 1 && h->T <= 256 && rbits <= 22 && h->sort_mode == 3;
   (void)sms0;
   // bucket plan (sort_mode 5): one pass on the top 8 key bits, then per-bucket local sorts
-  // (auto for large plans of small buckets -- <= 1024 keys per bucket on average: measured r02as,
-  // sweep P=1 plan 49.7 -> 32.5 us; DLRM-small, 1280 per bucket but a 5 K-key Zipf-hot bucket,
-  // 39.8 -> 43.2 us, so the plain plan stays the default there)
+  // Auto: 64 K..512 K lookups (<= 2 K keys per bucket on average) and <= 32 K lookups per table
+  // (the largest bucket holds a table's Zipf-hot row, ~10 % of its lookups, and the CTA sorting
+  // it bounds the kernel).  Measured r02bc (plan, plain -> bucket): sweep P=1 49.7 -> 27.2 us,
+  // weak 48.2 -> 42.4, sweep P=4 59.4 -> 56.3; DLRM-small (41 K lookups per table, a ~5 K-key
+  // bucket) 39.7 -> 51.3, so it keeps the plain plan.
   const bool bkt = kbits > 8 && (h->sort_mode == 5 ||
-                                 (h->sort_mode == 0 && n >= (1 << 16) && n <= 256 * 1024));
+                                 (h->sort_mode == 0 && n >= (1 << 16) && n <= (1 << 19) &&
+                                  n <= (int64_t)32768 * std::max(h->T, 1)));
   const int passes = seg ? 2 : bkt ? 1 : (kbits + 7) / 8;
   const int64_t nchunks = (n + kBwdChunkMin - 1) / kBwdChunkMin;   // upper bound
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;

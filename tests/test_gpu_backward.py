@@ -809,8 +809,8 @@ def test_bucket_plan_degenerate(case):
 @pytest.mark.parametrize("name", ["dlrm_small", "weak", "sweep_p1", "sweep_p8", "dlrm_wide"])
 def test_bucket_plan_full_size_equals_plain(name):
     """BASELINE configs at full size: the bucket plan's tables are bitwise those of the plain
-    plan (fp32 gradients: equal results need the same lookup order); sweep P=1 takes the bucket
-    plan by default (auto), the others are forced."""
+    plan (fp32 gradients: equal results need the same lookup order); weak and sweep P=1 take
+    the bucket plan by default (auto), the others are forced."""
     cfg = synth.config_for(name, W=1)
     idx_h, off_h = synth.gen_all_csr(cfg, 0)[0]
     rng = np.random.default_rng(1)
